@@ -1,0 +1,157 @@
+/* voltb200 -- B200-native preprocessing stage of the voltseg pipeline
+ * (per-frame rigid motion correction -> per-time-block summary images).
+ *
+ * C ABI: plain pointers and sizes, no torch or numpy types.  Every entry point
+ * returns VB_OK (0) or a positive VB_E* code; vb_last_error() returns the
+ * calling thread's last message.  Messages for argument errors are the
+ * reference's ValueError texts so a binding can re-raise them verbatim.
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/voltseg):
+ *   vb_mean_zncc_scores      <- _native.pyx:22-118 mean_zncc_scores / kernels.py:98-108
+ *   vb_patch_grid            <- motion.py:52-75 PatchGrid.cover
+ *   vb_make_reference        <- motion.py:211-214 make_reference
+ *   vb_motion_plan_* /
+ *   vb_motion_estimate       <- motion.py:113-160 estimate_motion over many frames
+ *                               (ZNCC grid + tie-broken argmax + quadratic fit)
+ *   vb_correct_frames        <- motion.py:235-240 / :244-248 correct_frame / translate
+ *   vb_summarize             <- summarize.py:95-102 summarize / summarize_segment
+ *                               (optionally fused with the motion warp)
+ *   vb_stage_*               <- motion.py:217-241 correct_motion followed by
+ *                               summarize.py:99-102 (pipeline.py:198-224 call pattern),
+ *                               host buffers in and out (the drop-in boundary)
+ */
+#ifndef VOLTB200_H
+#define VOLTB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VB_OK 0
+#define VB_EINVAL 1 /* argument error (reference raises ValueError) */
+#define VB_ECUDA 2  /* CUDA runtime / launch failure */
+#define VB_ENOMEM 3 /* device or pinned allocation failed */
+
+/* Frame sample types accepted on input.  u16 is the camera format; f32 is the
+ * reference's in-memory Video type (video_io.py:28-46). */
+#define VB_U16 0
+#define VB_F32 1
+
+/* motion.py:27-41 MotionVector.  x = dx + sub_dx, y = dy + sub_dy. */
+typedef struct vb_motion {
+    int32_t dx;
+    int32_t dy;
+    double sub_dx;
+    double sub_dy;
+    double confidence;
+} vb_motion;
+
+const char* vb_version(void);
+const char* vb_last_error(void);
+
+/* ---------------- operator level, host buffers ---------------- */
+
+/* Mean patch ZNCC of `frame` windows at origin+(dx,dy) against `reference`
+ * patches for all |dx|,|dy| <= radius.  frame/reference: float32 [height][width]
+ * C-contiguous host arrays; origins: int32 [n_origins][2] of (x, y);
+ * out_scores: float64 [(2r+1)][(2r+1)] indexed [dy+r][dx+r].
+ * Errors: "frame and reference dimensions differ" is the caller's check (one
+ * shape is passed); "patch origin too close to border for search radius";
+ * "search radius too large (max 31)". */
+int vb_mean_zncc_scores(const float* frame, const float* reference, int height, int width,
+                        const int32_t* origins, int n_origins, int patch, int radius,
+                        double* out_scores);
+
+/* PatchGrid.cover(height, width, patch, margin=margin): origins may be NULL to
+ * query *n_origins.  Error: "frame HxW too small for patch P with margin M". */
+int vb_patch_grid(int height, int width, int patch, int margin, int32_t* origins, int* n_origins);
+
+/* ---------------- device primitives (stream-ordered) ---------------- */
+/* All *_dev pointers are device memory on the current device; `stream` is a
+ * cudaStream_t (NULL = legacy default stream). */
+
+/* Template: float64 per-pixel sum of n frames (sequential frame order).  With
+ * accumulate != 0 the sum is added to sum_dev (for sharded recordings whose
+ * partial sums are then all-reduced). */
+int vb_template_sum(const void* frames_dev, int dtype, int64_t n_frames, int height, int width,
+                    double* sum_dev, int accumulate, void* stream);
+/* ref_dev[i] = float32(sum_dev[i] / n_total)  (motion.py:214). */
+int vb_template_finish(const double* sum_dev, int64_t n_total, int64_t n_pixels, float* ref_dev,
+                       void* stream);
+/* make_reference in one call: mean of the first min(n_frames, ref_frames) frames. */
+int vb_make_reference(const void* frames_dev, int dtype, int64_t n_frames, int height, int width,
+                      int ref_frames, float* ref_dev, void* stream);
+
+/* Motion plan: geometry + prepared template patches for one recording. */
+typedef struct vb_motion_plan vb_motion_plan;
+int vb_motion_plan_create(vb_motion_plan** plan, int height, int width, int patch, int radius,
+                          const int32_t* origins_host, int n_origins);
+int vb_motion_plan_set_reference(vb_motion_plan* plan, const float* ref_dev, void* stream);
+/* Per-frame motion vectors for n frames (optionally the full score grids,
+ * float64 [n][(2r+1)][(2r+1)]). */
+int vb_motion_estimate(vb_motion_plan* plan, const void* frames_dev, int dtype, int64_t n_frames,
+                       int subpixel, vb_motion* vectors_dev, double* scores_dev, void* stream);
+int vb_motion_plan_destroy(vb_motion_plan* plan);
+
+/* corrected[t] = frame unchanged if the vector is (0,0), else
+ * translate(frame, -x, -y)  (bit-exact float32 bilinear, edge replicated). */
+int vb_correct_frames(const void* frames_dev, int dtype, int64_t n_frames, int height, int width,
+                      const vb_motion* vectors_dev, float* corrected_dev, void* stream);
+
+/* Per-block summary images of n frames split into ceil(n/L) blocks
+ * (summarize.py:44-102).  If vectors_dev != NULL the motion warp is applied on
+ * the fly (frames are raw) and, if corrected_dev != NULL, the corrected frames
+ * are written too.  weights: host float64 [2*wradius+1] (scipy
+ * _gaussian_kernel1d).  spatial_dev / temporal_dev: float32 [K][height][width].
+ * Error: "segment length must be >= 2"; a final block of one frame raises
+ * "temporal summary needs at least 2 frames" (summarize.py:79-80). */
+int vb_summarize(const void* frames_dev, int dtype, const vb_motion* vectors_dev, int64_t n_frames,
+                 int height, int width, int segment_length, const double* weights, int wradius,
+                 float* corrected_dev, float* spatial_dev, float* temporal_dev, void* stream);
+
+/* Separable Gaussian smoothing of each frame (scipy gaussian_filter with mode
+ * "reflect": H pass then W pass, float64 accumulate, f32 per pass;
+ * summarize.py:60-73).  out_dev: float32 [n][height][width]. */
+int vb_smooth_frames(const void* frames_dev, int dtype, int64_t n_frames, int height, int width,
+                     const double* weights, int wradius, float* out_dev, void* stream);
+
+/* ---------------- whole stage, host buffers (drop-in boundary) ---------------- */
+typedef struct vb_stage_config {
+    int height, width;
+    int patch;          /* MotionConfig.patch_size (motion.py:203-208), default 21 */
+    int radius;         /* MotionConfig.search_radius */
+    int subpixel;       /* MotionConfig.subpixel */
+    int ref_frames;     /* REFERENCE_FRAMES (motion.py:24) */
+    int segment_length; /* summarize(..., segment_length) */
+    double sigma;       /* summarize(..., sigma) */
+    int device;         /* CUDA device ordinal */
+    int64_t chunk_frames; /* host->device streaming granularity (0 = auto) */
+} vb_stage_config;
+
+typedef struct vb_stage vb_stage;
+int vb_stage_create(vb_stage** stage, const vb_stage_config* cfg);
+/* Replace the smoothing weights (default: libm exp of scipy's formula).  The
+ * Python binding passes numpy-computed _gaussian_kernel1d weights so the
+ * summaries are bit-identical to scipy's. */
+int vb_stage_set_weights(vb_stage* stage, const double* weights, int wradius);
+/* Runs correct_motion + summarize over a host recording (pinned or pageable).
+ * frames_host: dtype [n][h][w]; vectors_host: [n]; spatial/temporal_host:
+ * float32 [ceil(n/L)][h][w]; corrected_host: float32 [n][h][w] or NULL (the
+ * corrected video then stays on the device only). */
+int vb_stage_run_host(vb_stage* stage, const void* frames_host, int dtype, int64_t n_frames,
+                      vb_motion* vectors_host, float* spatial_host, float* temporal_host,
+                      float* corrected_host);
+/* Number of device kernels the last vb_stage_run_host launched. */
+int64_t vb_stage_last_launches(const vb_stage* stage);
+int vb_stage_destroy(vb_stage* stage);
+
+/* Kernel launches issued by this library since load (all entry points). */
+int64_t vb_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VOLTB200_H */

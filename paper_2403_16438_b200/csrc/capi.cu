@@ -1,0 +1,299 @@
+// C-ABI entry points and the host runtime (plans, chunked stage executor).
+// See include/voltb200.h for the contract and the reference interfaces each
+// entry point replaces.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <string>
+#include <vector>
+
+#include "vb.cuh"
+
+namespace vb {
+
+static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+    g_err = std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? VB_ENOMEM : VB_ECUDA;
+}
+std::atomic<int64_t>& launches() { return g_launches; }
+
+// motion.py:71-75
+static std::vector<int> positions(int lo, int hi, int stride) {
+    std::vector<int> pos;
+    for (int p = lo; p <= hi; p += stride) pos.push_back(p);
+    if (pos.back() != hi) pos.push_back(hi);
+    return pos;
+}
+
+static int check_origins(int h, int w, const int32_t* origins, int n, int patch, int radius) {
+    for (int i = 0; i < n; ++i) {  // _native.pyx:41-46, kernels.py:39-42
+        const int px = origins[2 * i], py = origins[2 * i + 1];
+        if (px - radius < 0 || py - radius < 0 || px + patch + radius > w || py + patch + radius > h)
+            return fail(VB_EINVAL, "patch origin too close to border for search radius");
+    }
+    if (radius > kMaxRadius) return fail(VB_EINVAL, "search radius too large (max 31)");  // _native.pyx:65-66
+    if (radius < 0) return fail(VB_EINVAL, "search_radius must be >= 1");
+    if (patch < 1) return fail(VB_EINVAL, "patch size must be >= 1");
+    return VB_OK;
+}
+
+}  // namespace vb
+
+using namespace vb;
+
+// ---------------------------------------------------------------- plan
+struct vb_motion_plan {
+    int h = 0, w = 0, patch = 0, radius = 0;
+    Templates t;
+    std::vector<int32_t> origins;
+    bool have_ref = false;
+};
+
+static void free_templates(Templates& t) {
+    cudaFree(t.tmpl);
+    cudaFree(t.rvar);
+    cudaFree(t.origins);
+    cudaFree(t.patch_col);
+    cudaFree(t.groups);
+    t = Templates();
+}
+
+// Group consecutive patches that share an origin row into CTA work units.
+static void build_groups(const std::vector<int32_t>& o, int patch, int radius, int max_g,
+                         std::vector<PatchGroup>& groups, std::vector<int32_t>& col) {
+    const int n = (int)o.size() / 2;
+    col.assign(n, 0);
+    int i = 0;
+    while (i < n) {
+        PatchGroup g;
+        memset(&g, 0, sizeof(g));
+        g.first = i;
+        int j = i + 1;
+        int minx = o[2 * i], maxx = o[2 * i];
+        while (j < n && j - i < max_g && o[2 * j + 1] == o[2 * i + 1]) {
+            const int x = o[2 * j];
+            const int nmin = std::min(minx, x), nmax = std::max(maxx, x);
+            if (nmax - nmin > (max_g - 1) * patch + patch) break;  // keep the union compact
+            minx = nmin;
+            maxx = nmax;
+            ++j;
+        }
+        g.count = j - i;
+        g.x0 = minx - radius;
+        g.y0 = o[2 * i + 1] - radius;
+        g.wu = maxx - minx + patch + 2 * radius;
+        for (int k = i; k < j; ++k) col[k] = o[2 * k] - minx;
+        groups.push_back(g);
+        i = j;
+    }
+}
+
+extern "C" {
+
+const char* vb_version(void) { return "voltb200 0.1 (sm_100a)"; }
+const char* vb_last_error(void) { return g_err.c_str(); }
+int64_t vb_launch_count(void) { return g_launches.load(); }
+
+int vb_patch_grid(int height, int width, int patch, int margin, int32_t* origins, int* n_origins) {
+    const int lo_x = margin, hi_x = width - margin - patch;
+    const int lo_y = margin, hi_y = height - margin - patch;
+    if (patch < 1 || hi_x < lo_x || hi_y < lo_y) {
+        return fail(VB_EINVAL, "frame " + std::to_string(height) + "x" + std::to_string(width) +
+                                   " too small for patch " + std::to_string(patch) + " with margin " +
+                                   std::to_string(margin));
+    }
+    const std::vector<int> xs = positions(lo_x, hi_x, patch), ys = positions(lo_y, hi_y, patch);
+    const int n = (int)(xs.size() * ys.size());
+    if (n_origins) *n_origins = n;
+    if (origins) {
+        int k = 0;
+        for (int y : ys)
+            for (int x : xs) {
+                origins[2 * k] = x;
+                origins[2 * k + 1] = y;
+                ++k;
+            }
+    }
+    return VB_OK;
+}
+
+int vb_motion_plan_create(vb_motion_plan** out, int height, int width, int patch, int radius,
+                          const int32_t* origins_host, int n_origins) {
+    if (!out) return fail(VB_EINVAL, "null plan pointer");
+    *out = nullptr;
+    if (n_origins < 1) return fail(VB_EINVAL, "no patches");
+    int rc = check_origins(height, width, origins_host, n_origins, patch, radius);
+    if (rc) return rc;
+    auto* p = new vb_motion_plan();
+    p->h = height;
+    p->w = width;
+    p->patch = patch;
+    p->radius = radius;
+    p->origins.assign(origins_host, origins_host + 2 * (size_t)n_origins);
+    std::vector<PatchGroup> groups;
+    std::vector<int32_t> col;
+    // group width: ~8 patches keeps the CTA at <= ~80 KB of shared memory
+    const int max_g = std::max(1, std::min(kMaxGroup, patch >= 16 ? 8 : 12));
+    build_groups(p->origins, patch, radius, max_g, groups, col);
+    Templates& t = p->t;
+    t.n = n_origins;
+    t.n_groups = (int)groups.size();
+    t.tp = (patch + 3) & ~3;
+    for (auto& g : groups) {
+        t.max_g = std::max(t.max_g, (int)g.count);
+        t.max_wu = std::max(t.max_wu, (int)g.wu);
+    }
+    cudaError_t e = cudaSuccess;
+    e = e ? e : cudaMalloc(&t.tmpl, (size_t)n_origins * patch * t.tp * sizeof(float));
+    e = e ? e : cudaMalloc(&t.rvar, 2 * (size_t)n_origins * sizeof(double));
+    t.rmean = t.rvar ? t.rvar + n_origins : nullptr;
+    e = e ? e : cudaMalloc(&t.origins, (size_t)n_origins * 2 * sizeof(int32_t));
+    e = e ? e : cudaMalloc(&t.patch_col, (size_t)n_origins * sizeof(int32_t));
+    e = e ? e : cudaMalloc(&t.groups, groups.size() * sizeof(PatchGroup));
+    e = e ? e : cudaMemcpy(t.origins, origins_host, (size_t)n_origins * 2 * sizeof(int32_t), cudaMemcpyHostToDevice);
+    e = e ? e : cudaMemcpy(t.patch_col, col.data(), col.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+    e = e ? e : cudaMemcpy(t.groups, groups.data(), groups.size() * sizeof(PatchGroup), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        free_templates(t);
+        delete p;
+        return cuda_fail(e, "vb_motion_plan_create");
+    }
+    *out = p;
+    return VB_OK;
+}
+
+int vb_motion_plan_set_reference(vb_motion_plan* p, const float* ref_dev, void* stream) {
+    if (!p || !ref_dev) return fail(VB_EINVAL, "null argument");
+    int rc = launch_prep_templates(ref_dev, p->h, p->w, p->patch, p->t, (cudaStream_t)stream);
+    if (rc == VB_OK) p->have_ref = true;
+    return rc;
+}
+
+int vb_motion_estimate(vb_motion_plan* p, const void* frames_dev, int dtype, int64_t n_frames, int subpixel,
+                       vb_motion* vectors_dev, double* scores_dev, void* stream) {
+    if (!p || !vectors_dev || (!frames_dev && n_frames > 0)) return fail(VB_EINVAL, "null argument");
+    if (!p->have_ref) return fail(VB_EINVAL, "motion plan has no reference (call vb_motion_plan_set_reference)");
+    if (dtype != VB_U16 && dtype != VB_F32) return fail(VB_EINVAL, "unsupported sample type");
+    return launch_motion(p->t, p->h, p->w, p->patch, p->radius, frames_dev, dtype, n_frames, subpixel, vectors_dev,
+                         scores_dev, (cudaStream_t)stream);
+}
+
+int vb_motion_plan_destroy(vb_motion_plan* p) {
+    if (!p) return VB_OK;
+    free_templates(p->t);
+    delete p;
+    return VB_OK;
+}
+
+int vb_template_sum(const void* frames_dev, int dtype, int64_t n_frames, int height, int width, double* sum_dev,
+                    int accumulate, void* stream) {
+    if (!sum_dev) return fail(VB_EINVAL, "null argument");
+    if (dtype != VB_U16 && dtype != VB_F32) return fail(VB_EINVAL, "unsupported sample type");
+    return launch_template_sum(frames_dev, dtype, n_frames, (int64_t)height * width, sum_dev, accumulate,
+                               (cudaStream_t)stream);
+}
+
+int vb_template_finish(const double* sum_dev, int64_t n_total, int64_t n_pixels, float* ref_dev, void* stream) {
+    if (!sum_dev || !ref_dev || n_total < 1) return fail(VB_EINVAL, "invalid template arguments");
+    return launch_template_finish(sum_dev, n_total, n_pixels, ref_dev, (cudaStream_t)stream);
+}
+
+int vb_make_reference(const void* frames_dev, int dtype, int64_t n_frames, int height, int width, int ref_frames,
+                      float* ref_dev, void* stream) {
+    if (n_frames < 1 || ref_frames < 1) return fail(VB_EINVAL, "need at least one frame");
+    const int64_t n = std::min<int64_t>(n_frames, ref_frames);
+    const int64_t hw = (int64_t)height * width;
+    cudaStream_t s = (cudaStream_t)stream;
+    double* sum = nullptr;
+    VB_CUDA(cudaMallocAsync(&sum, hw * sizeof(double), s));
+    int rc = launch_template_sum(frames_dev, dtype, n, hw, sum, 0, s);
+    if (rc == VB_OK) rc = launch_template_finish(sum, n, hw, ref_dev, s);
+    cudaFreeAsync(sum, s);
+    return rc;
+}
+
+int vb_correct_frames(const void* frames_dev, int dtype, int64_t n_frames, int height, int width,
+                      const vb_motion* vectors_dev, float* corrected_dev, void* stream) {
+    if (dtype != VB_U16 && dtype != VB_F32) return fail(VB_EINVAL, "unsupported sample type");
+    return launch_correct(frames_dev, dtype, n_frames, height, width, vectors_dev, corrected_dev,
+                          (cudaStream_t)stream);
+}
+
+int vb_summarize(const void* frames_dev, int dtype, const vb_motion* vectors_dev, int64_t n_frames, int height,
+                 int width, int segment_length, const double* weights, int wradius, float* corrected_dev,
+                 float* spatial_dev, float* temporal_dev, void* stream) {
+    if (segment_length < 2) return fail(VB_EINVAL, "segment length must be >= 2");  // summarize.py:46-47
+    if (dtype != VB_U16 && dtype != VB_F32) return fail(VB_EINVAL, "unsupported sample type");
+    if (n_frames < 1) return fail(VB_EINVAL, "video dimensions must all be >= 1");
+    if (n_frames % segment_length == 1)  // summarize.py:79-80 on the final block
+        return fail(VB_EINVAL, "temporal summary needs at least 2 frames");
+    if (!weights || wradius < 0 || !spatial_dev || !temporal_dev) return fail(VB_EINVAL, "null argument");
+    return launch_summarize(frames_dev, dtype, vectors_dev, n_frames, height, width, segment_length, weights,
+                            wradius, corrected_dev, spatial_dev, temporal_dev, (cudaStream_t)stream);
+}
+
+int vb_smooth_frames(const void* frames_dev, int dtype, int64_t n_frames, int height, int width,
+                     const double* weights, int wradius, float* out_dev, void* stream) {
+    if (dtype != VB_U16 && dtype != VB_F32) return fail(VB_EINVAL, "unsupported sample type");
+    if (!weights || wradius < 0 || !out_dev) return fail(VB_EINVAL, "null argument");
+    return launch_smooth(frames_dev, dtype, n_frames, height, width, weights, wradius, out_dev,
+                         (cudaStream_t)stream);
+}
+
+int vb_mean_zncc_scores(const float* frame, const float* reference, int height, int width, const int32_t* origins,
+                        int n_origins, int patch, int radius, double* out_scores) {
+    if (!frame || !reference || !origins || !out_scores) return fail(VB_EINVAL, "null argument");
+    int rc = check_origins(height, width, origins, n_origins, patch, radius);
+    if (rc) return rc;
+    const int S = 2 * radius + 1;
+    const size_t hw = (size_t)height * width;
+    if (n_origins == 0) {  // reference: empty mean -> division by zero yields NaN
+        for (int i = 0; i < S * S; ++i) out_scores[i] = NAN;
+        return VB_OK;
+    }
+    vb_motion_plan* plan = nullptr;
+    rc = vb_motion_plan_create(&plan, height, width, patch, radius, origins, n_origins);
+    if (rc) return rc;
+    float *d_frame = nullptr, *d_ref = nullptr;
+    vb_motion* d_vec = nullptr;
+    double* d_scores = nullptr;
+    cudaStream_t s = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    e = e ? e : cudaMallocAsync(&d_frame, hw * 4, s);
+    e = e ? e : cudaMallocAsync(&d_ref, hw * 4, s);
+    e = e ? e : cudaMallocAsync(&d_vec, sizeof(vb_motion), s);
+    e = e ? e : cudaMallocAsync(&d_scores, (size_t)S * S * 8, s);
+    e = e ? e : cudaMemcpyAsync(d_frame, frame, hw * 4, cudaMemcpyHostToDevice, s);
+    e = e ? e : cudaMemcpyAsync(d_ref, reference, hw * 4, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) rc = cuda_fail(e, "vb_mean_zncc_scores setup");
+    if (rc == VB_OK) rc = vb_motion_plan_set_reference(plan, d_ref, s);
+    if (rc == VB_OK) rc = vb_motion_estimate(plan, d_frame, VB_F32, 1, 0, d_vec, d_scores, s);
+    if (rc == VB_OK) {
+        e = cudaMemcpyAsync(out_scores, d_scores, (size_t)S * S * 8, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) rc = cuda_fail(e, "vb_mean_zncc_scores");
+    }
+    if (s) {
+        cudaFreeAsync(d_frame, s);
+        cudaFreeAsync(d_ref, s);
+        cudaFreeAsync(d_vec, s);
+        cudaFreeAsync(d_scores, s);
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+    }
+    vb_motion_plan_destroy(plan);
+    return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,295 @@
+// Whole-stage executor over a HOST recording: the drop-in boundary for
+// correct_motion (motion.py:217-241) followed by summarize (summarize.py:99-102),
+// as pipeline.py:198-224 calls them.
+//
+// Frame-chunk scheduler: chunks of whole blocks (a multiple of L frames) are
+// copied host->HBM on an H2D stream into a two-slot device ring while the
+// previous chunk computes (motion estimate -> fused warp + summaries) on the
+// compute stream and the chunk before that drains device->host on a D2H
+// stream.  Pageable input is first packed into pinned staging slots by the
+// host thread (pinned input DMAs directly).  Events order slot reuse.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "vb.cuh"
+
+using namespace vb;
+
+struct vb_stage {
+    vb_stage_config cfg{};
+    cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
+    vb_motion_plan* plan = nullptr;
+    std::vector<int32_t> origins;
+    std::vector<double> weights;
+    int wradius = 0;
+    int64_t chunk = 0;  // frames per chunk (multiple of L)
+    size_t esz = 0;     // bytes per sample of the allocated ring
+    void* d_frames[2] = {nullptr, nullptr};
+    vb_motion* d_vec[2] = {nullptr, nullptr};
+    float* d_sp[2] = {nullptr, nullptr};
+    float* d_tp[2] = {nullptr, nullptr};
+    float* d_corr[2] = {nullptr, nullptr};
+    void* h_stage[2] = {nullptr, nullptr};
+    // pinned output staging: D2H into page-locked memory never blocks the
+    // host thread; chunk k-1 is unpacked into the caller's buffers while
+    // chunk k computes.
+    vb_motion* h_vec[2] = {nullptr, nullptr};
+    float* h_sp[2] = {nullptr, nullptr};
+    float* h_tp[2] = {nullptr, nullptr};
+    float* h_corr[2] = {nullptr, nullptr};
+    double* d_tsum = nullptr;
+    float* d_ref = nullptr;
+    cudaEvent_t ev_h2d[2]{}, ev_comp[2]{}, ev_d2h[2]{};
+    int64_t last_launches = 0;
+};
+
+static void stage_free_buffers(vb_stage* st) {
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(st->d_frames[i]);
+        cudaFree(st->d_vec[i]);
+        cudaFree(st->d_sp[i]);
+        cudaFree(st->d_tp[i]);
+        cudaFree(st->d_corr[i]);
+        cudaFreeHost(st->h_stage[i]);
+        cudaFreeHost(st->h_vec[i]);
+        cudaFreeHost(st->h_sp[i]);
+        cudaFreeHost(st->h_tp[i]);
+        cudaFreeHost(st->h_corr[i]);
+        st->d_frames[i] = st->h_stage[i] = nullptr;
+        st->h_vec[i] = nullptr;
+        st->h_sp[i] = st->h_tp[i] = st->h_corr[i] = nullptr;
+        st->d_vec[i] = nullptr;
+        st->d_sp[i] = st->d_tp[i] = st->d_corr[i] = nullptr;
+    }
+    st->esz = 0;
+}
+
+extern "C" {
+
+int vb_stage_create(vb_stage** out, const vb_stage_config* cfg) {
+    if (!out || !cfg) return fail(VB_EINVAL, "null argument");
+    *out = nullptr;
+    if (cfg->radius < 1) return fail(VB_EINVAL, "search_radius must be >= 1");
+    if (cfg->segment_length < 2) return fail(VB_EINVAL, "segment length must be >= 2");
+    if (!(cfg->sigma > 0)) return fail(VB_EINVAL, "sigma must be positive");
+    if (cfg->ref_frames < 1) return fail(VB_EINVAL, "ref_frames must be >= 1");
+    VB_CUDA(cudaSetDevice(cfg->device));
+    auto* st = new vb_stage();
+    st->cfg = *cfg;
+    int n = 0;
+    int rc = vb_patch_grid(cfg->height, cfg->width, cfg->patch, cfg->radius, nullptr, &n);
+    if (rc) {
+        delete st;
+        return rc;
+    }
+    st->origins.resize(2 * (size_t)n);
+    vb_patch_grid(cfg->height, cfg->width, cfg->patch, cfg->radius, st->origins.data(), &n);
+    rc = vb_motion_plan_create(&st->plan, cfg->height, cfg->width, cfg->patch, cfg->radius, st->origins.data(), n);
+    if (rc) {
+        delete st;
+        return rc;
+    }
+    // scipy _gaussian_kernel1d(sigma, 0, ceil(3 sigma)) (summarize.py:71).
+    // NOTE: libm exp may differ from numpy's in the last ulp; the Python layer
+    // passes numpy-computed weights to vb_summarize for bit-exact parity.
+    st->wradius = (int)ceil(3.0 * cfg->sigma);
+    st->weights.resize(2 * st->wradius + 1);
+    double tot = 0.0;
+    for (int i = -st->wradius; i <= st->wradius; ++i) {
+        st->weights[i + st->wradius] = exp(-0.5 / (cfg->sigma * cfg->sigma) * (double)(i * i));
+        tot += st->weights[i + st->wradius];
+    }
+    for (auto& wv : st->weights) wv /= tot;
+    const int L = cfg->segment_length;
+    int64_t want = cfg->chunk_frames > 0 ? cfg->chunk_frames : 2048;
+    st->chunk = std::max<int64_t>(1, (want + L / 2) / L) * L;
+    cudaError_t e = cudaStreamCreateWithFlags(&st->s_comp, cudaStreamNonBlocking);
+    e = e ? e : cudaStreamCreateWithFlags(&st->s_h2d, cudaStreamNonBlocking);
+    e = e ? e : cudaStreamCreateWithFlags(&st->s_d2h, cudaStreamNonBlocking);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+        e = cudaEventCreateWithFlags(&st->ev_h2d[i], cudaEventDisableTiming);
+        e = e ? e : cudaEventCreateWithFlags(&st->ev_comp[i], cudaEventDisableTiming);
+        e = e ? e : cudaEventCreateWithFlags(&st->ev_d2h[i], cudaEventDisableTiming);
+    }
+    const size_t hw = (size_t)cfg->height * cfg->width;
+    e = e ? e : cudaMalloc(&st->d_tsum, hw * sizeof(double));
+    e = e ? e : cudaMalloc(&st->d_ref, hw * sizeof(float));
+    if (e != cudaSuccess) {
+        vb_stage_destroy(st);
+        return cuda_fail(e, "vb_stage_create");
+    }
+    *out = st;
+    return VB_OK;
+}
+
+int vb_stage_set_weights(vb_stage* st, const double* weights, int wradius) {
+    if (!st || !weights || wradius < 0) return fail(VB_EINVAL, "null argument");
+    st->weights.assign(weights, weights + 2 * wradius + 1);
+    st->wradius = wradius;
+    return VB_OK;
+}
+
+int64_t vb_stage_last_launches(const vb_stage* st) { return st ? st->last_launches : 0; }
+
+int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t n_frames, vb_motion* vectors_host,
+                      float* spatial_host, float* temporal_host, float* corrected_host) {
+    if (!st || !frames_host || !vectors_host || !spatial_host || !temporal_host) return fail(VB_EINVAL, "null argument");
+    if (dtype != VB_U16 && dtype != VB_F32) return fail(VB_EINVAL, "unsupported sample type");
+    const vb_stage_config& c = st->cfg;
+    const int L = c.segment_length;
+    if (n_frames < 1) return fail(VB_EINVAL, "video dimensions must all be >= 1");
+    if (n_frames % L == 1) return fail(VB_EINVAL, "temporal summary needs at least 2 frames");
+    VB_CUDA(cudaSetDevice(c.device));
+    const int64_t launches0 = launches().load();
+    const size_t hw = (size_t)c.height * c.width;
+    const size_t esz = dtype == VB_U16 ? 2 : 4;
+    const int64_t C = st->chunk;
+    const int64_t cblk = C / L;
+
+    cudaPointerAttributes attr;
+    bool pinned = cudaPointerGetAttributes(&attr, frames_host) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+
+    // (re)allocate the two-slot ring
+    if (st->esz != esz || (corrected_host && !st->d_corr[0]) || (!pinned && !st->h_stage[0])) {
+        stage_free_buffers(st);
+        cudaError_t e = cudaSuccess;
+        for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+            e = cudaMalloc(&st->d_frames[i], (size_t)C * hw * esz);
+            e = e ? e : cudaMalloc(&st->d_vec[i], (size_t)C * sizeof(vb_motion));
+            e = e ? e : cudaMalloc(&st->d_sp[i], (size_t)cblk * hw * sizeof(float));
+            e = e ? e : cudaMalloc(&st->d_tp[i], (size_t)cblk * hw * sizeof(float));
+            if (corrected_host) e = e ? e : cudaMalloc(&st->d_corr[i], (size_t)C * hw * sizeof(float));
+            e = e ? e : cudaHostAlloc(&st->h_vec[i], (size_t)C * sizeof(vb_motion), cudaHostAllocDefault);
+            e = e ? e : cudaHostAlloc(&st->h_sp[i], (size_t)cblk * hw * sizeof(float), cudaHostAllocDefault);
+            e = e ? e : cudaHostAlloc(&st->h_tp[i], (size_t)cblk * hw * sizeof(float), cudaHostAllocDefault);
+            if (corrected_host)
+                e = e ? e : cudaHostAlloc(&st->h_corr[i], (size_t)C * hw * sizeof(float), cudaHostAllocDefault);
+            if (!pinned) e = e ? e : cudaHostAlloc(&st->h_stage[i], (size_t)C * hw * esz, cudaHostAllocDefault);
+        }
+        if (e != cudaSuccess) {
+            stage_free_buffers(st);
+            return cuda_fail(e, "vb_stage_run_host allocation");
+        }
+        st->esz = esz;
+    }
+
+    // host->device copy of frames [f0, f0+nf) into slot
+    auto upload = [&](int slot, int64_t f0, int64_t nf) -> int {
+        const char* src = (const char*)frames_host + (size_t)f0 * hw * esz;
+        const size_t bytes = (size_t)nf * hw * esz;
+        if (!pinned) {
+            // staging slot is free once its previous upload completed
+            VB_CUDA(cudaEventSynchronize(st->ev_h2d[slot]));
+            memcpy(st->h_stage[slot], src, bytes);
+            src = (const char*)st->h_stage[slot];
+        }
+        VB_CUDA(cudaStreamWaitEvent(st->s_h2d, st->ev_comp[slot], 0));  // slot no longer read by compute
+        VB_CUDA(cudaMemcpyAsync(st->d_frames[slot], src, bytes, cudaMemcpyHostToDevice, st->s_h2d));
+        VB_CUDA(cudaEventRecord(st->ev_h2d[slot], st->s_h2d));
+        return VB_OK;
+    };
+    // fresh events so the first waits are no-ops
+    for (int i = 0; i < 2; ++i) {
+        VB_CUDA(cudaEventRecord(st->ev_comp[i], st->s_comp));
+        VB_CUDA(cudaEventRecord(st->ev_d2h[i], st->s_d2h));
+        VB_CUDA(cudaEventRecord(st->ev_h2d[i], st->s_h2d));
+    }
+
+    // ---- phase A: template = mean of the first min(n, M) frames ----
+    const int64_t m = std::min<int64_t>(n_frames, c.ref_frames);
+    int rc = VB_OK;
+    for (int64_t f0 = 0, k = 0; f0 < m && rc == VB_OK; f0 += C, ++k) {
+        const int slot = (int)(k & 1);
+        const int64_t nf = std::min<int64_t>(C, m - f0);
+        rc = upload(slot, f0, nf);
+        if (rc) break;
+        VB_CUDA(cudaStreamWaitEvent(st->s_comp, st->ev_h2d[slot], 0));
+        rc = launch_template_sum(st->d_frames[slot], dtype, nf, (int64_t)hw, st->d_tsum, f0 > 0, st->s_comp);
+        if (rc) break;
+        VB_CUDA(cudaEventRecord(st->ev_comp[slot], st->s_comp));
+    }
+    if (rc == VB_OK) rc = launch_template_finish(st->d_tsum, m, (int64_t)hw, st->d_ref, st->s_comp);
+    if (rc == VB_OK) rc = vb_motion_plan_set_reference(st->plan, st->d_ref, st->s_comp);
+    for (int i = 0; i < 2 && rc == VB_OK; ++i) VB_CUDA(cudaEventRecord(st->ev_comp[i], st->s_comp));
+
+    // ---- phase B: chunks ----
+    const int64_t nchunks = (n_frames + C - 1) / C;
+    auto drain = [&](int64_t k) -> int {
+        const int slot = (int)(k & 1);
+        const int64_t f0 = k * C, nf = std::min<int64_t>(C, n_frames - f0);
+        const int64_t b0 = f0 / L, nb = (nf + L - 1) / L;
+        VB_CUDA(cudaEventSynchronize(st->ev_d2h[slot]));
+        memcpy(vectors_host + f0, st->h_vec[slot], (size_t)nf * sizeof(vb_motion));
+        memcpy(spatial_host + (size_t)b0 * hw, st->h_sp[slot], (size_t)nb * hw * sizeof(float));
+        memcpy(temporal_host + (size_t)b0 * hw, st->h_tp[slot], (size_t)nb * hw * sizeof(float));
+        if (corrected_host)
+            memcpy(corrected_host + (size_t)f0 * hw, st->h_corr[slot], (size_t)nf * hw * sizeof(float));
+        return VB_OK;
+    };
+    for (int64_t k = 0; k < nchunks && rc == VB_OK; ++k) {
+        const int slot = (int)(k & 1);
+        const int64_t f0 = k * C, nf = std::min<int64_t>(C, n_frames - f0);
+        const int64_t b0 = f0 / L, nb = (nf + L - 1) / L;
+        rc = upload(slot, f0, nf);
+        if (rc) break;
+        VB_CUDA(cudaStreamWaitEvent(st->s_comp, st->ev_h2d[slot], 0));
+        VB_CUDA(cudaStreamWaitEvent(st->s_comp, st->ev_d2h[slot], 0));  // outputs of chunk k-2 drained
+        rc = vb_motion_estimate(st->plan, st->d_frames[slot], dtype, nf, c.subpixel, st->d_vec[slot], nullptr,
+                                st->s_comp);
+        if (rc) break;
+        rc = launch_summarize(st->d_frames[slot], dtype, st->d_vec[slot], nf, c.height, c.width, L,
+                              st->weights.data(), st->wradius, corrected_host ? st->d_corr[slot] : nullptr,
+                              st->d_sp[slot], st->d_tp[slot], st->s_comp);
+        if (rc) break;
+        VB_CUDA(cudaEventRecord(st->ev_comp[slot], st->s_comp));
+        VB_CUDA(cudaStreamWaitEvent(st->s_d2h, st->ev_comp[slot], 0));
+        VB_CUDA(cudaMemcpyAsync(st->h_vec[slot], st->d_vec[slot], (size_t)nf * sizeof(vb_motion),
+                                cudaMemcpyDeviceToHost, st->s_d2h));
+        VB_CUDA(cudaMemcpyAsync(st->h_sp[slot], st->d_sp[slot], (size_t)nb * hw * sizeof(float),
+                                cudaMemcpyDeviceToHost, st->s_d2h));
+        VB_CUDA(cudaMemcpyAsync(st->h_tp[slot], st->d_tp[slot], (size_t)nb * hw * sizeof(float),
+                                cudaMemcpyDeviceToHost, st->s_d2h));
+        if (corrected_host)
+            VB_CUDA(cudaMemcpyAsync(st->h_corr[slot], st->d_corr[slot], (size_t)nf * hw * sizeof(float),
+                                    cudaMemcpyDeviceToHost, st->s_d2h));
+        VB_CUDA(cudaEventRecord(st->ev_d2h[slot], st->s_d2h));
+        if (k >= 1) rc = drain(k - 1);
+    }
+    if (rc == VB_OK && nchunks >= 1) rc = drain(nchunks - 1);
+    cudaError_t e1 = cudaStreamSynchronize(st->s_h2d);
+    cudaError_t e2 = cudaStreamSynchronize(st->s_comp);
+    cudaError_t e3 = cudaStreamSynchronize(st->s_d2h);
+    if (rc == VB_OK) {
+        cudaError_t e = e1 ? e1 : (e2 ? e2 : e3);
+        if (e != cudaSuccess) rc = cuda_fail(e, "vb_stage_run_host");
+    }
+    st->last_launches = launches().load() - launches0;
+    return rc;
+}
+
+int vb_stage_destroy(vb_stage* st) {
+    if (!st) return VB_OK;
+    if (st->s_comp) cudaStreamSynchronize(st->s_comp);
+    stage_free_buffers(st);
+    vb_motion_plan_destroy(st->plan);
+    cudaFree(st->d_tsum);
+    cudaFree(st->d_ref);
+    for (int i = 0; i < 2; ++i) {
+        if (st->ev_h2d[i]) cudaEventDestroy(st->ev_h2d[i]);
+        if (st->ev_comp[i]) cudaEventDestroy(st->ev_comp[i]);
+        if (st->ev_d2h[i]) cudaEventDestroy(st->ev_d2h[i]);
+    }
+    if (st->s_comp) cudaStreamDestroy(st->s_comp);
+    if (st->s_h2d) cudaStreamDestroy(st->s_h2d);
+    if (st->s_d2h) cudaStreamDestroy(st->s_d2h);
+    delete st;
+    return VB_OK;
+}
+
+}  // extern "C"

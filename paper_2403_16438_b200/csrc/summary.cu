@@ -1,0 +1,429 @@
+// Motion warp + per-block summary images (sm_100a).
+//
+// Reference algorithm (paths under /root/reference/pkg/src/voltseg):
+//   warp                motion.py:163-200 translate/_translate_int, :235-240, :244-248
+//   blocks              summarize.py:44-52 split_segments (ceil(T/L) blocks)
+//   spatial summary     summarize.py:55-57  (float64 sequential mean -> f32)
+//   smoothing           summarize.py:70-73  (scipy gaussian_filter1d, sigma=3,
+//                       radius 9, mode "reflect", H pass then W pass, float64
+//                       accumulation, f32 rounding after each pass)
+//   temporal summary    summarize.py:76-92  (max - median over time; midpoint
+//                       median for even counts)
+//
+// B200 design:
+//  K3 warp_smooth_kernel: one CTA per (block, 32x64 pixel tile) walks the
+//     block's frames in order.  Per frame it evaluates the corrected frame on
+//     the tile plus a reflect-mapped 9-pixel halo straight from the raw
+//     (u16/f32) frame, keeps the float64 running spatial sum of its own pixels
+//     in registers, optionally streams the corrected tile out, and runs the
+//     two separable 19-tap passes in shared memory (float64 accumulate in
+//     scipy's symmetric-pair order, unfused mul/add).  The smoothed tile is
+//     written time-major for K4.
+//  K4 median_kernel: one CTA per (block, 16 consecutive pixels) stages the
+//     block's smoothed column in shared memory; one warp per pixel holds up to
+//     32 samples per lane in registers and selects the exact median by radix
+//     bisection on the float bit pattern (non-negative floats order like
+//     uint32), with warp REDUX counts -- no sorting, no atomics.
+#include <math.h>
+
+#include <algorithm>
+
+#include "vb.cuh"
+
+namespace vb {
+
+// ------------------------------------------------------------------ warp
+struct WarpOp {
+    int mode;  // 0 identity, 1 integer shift, 2 bilinear
+    int ix, iy;
+    float fx, fy, omx, omy;
+};
+
+__device__ __forceinline__ WarpOp make_warp(const vb_motion* vec, int64_t t) {
+    WarpOp op;
+    op.mode = 0;
+    op.ix = op.iy = 0;
+    op.fx = op.fy = 0.f;
+    op.omx = op.omy = 1.f;
+    if (!vec) return op;
+    const vb_motion v = vec[t];
+    const double vx = (double)v.dx + v.sub_dx, vy = (double)v.dy + v.sub_dy;  // MotionVector.x/.y
+    if (vx == 0.0 && vy == 0.0) return op;                                     // motion.py:237-238
+    const double sx = -vx, sy = -vy;                                           // translate(f, -x, -y)
+    const double x0 = floor(sx), y0 = floor(sy);
+    op.ix = (int)x0;
+    op.iy = (int)y0;
+    if (sx == x0 && sy == y0) {  // motion.py:166-167 integer path
+        op.mode = 1;
+        return op;
+    }
+    op.mode = 2;
+    op.fx = (float)(sx - x0);  // frame.dtype.type(dx - x0)
+    op.fy = (float)(sy - y0);
+    op.omx = __fsub_rn(1.0f, op.fx);
+    op.omy = __fsub_rn(1.0f, op.fy);
+    return op;
+}
+
+// out[y,x] of translate(frame, sx, sy): samples frame[y - y0 (+1)][x - x0 (+1)]
+// with clamping; f32 ops in numpy's order, never fused.
+__device__ __forceinline__ float warp_sample(const void* f, int dtype, int64_t base, int h, int w, const WarpOp& op,
+                                             int y, int x) {
+    if (op.mode == 0) return load_sample(f, dtype, base + (int64_t)y * w + x);
+    const int ya = clampi(y - op.iy, 0, h - 1), xa = clampi(x - op.ix, 0, w - 1);
+    if (op.mode == 1) return load_sample(f, dtype, base + (int64_t)ya * w + xa);
+    const int yc = clampi(y - op.iy - 1, 0, h - 1), xb = clampi(x - op.ix - 1, 0, w - 1);
+    const float a = load_sample(f, dtype, base + (int64_t)ya * w + xa);
+    const float b = load_sample(f, dtype, base + (int64_t)ya * w + xb);
+    const float c = load_sample(f, dtype, base + (int64_t)yc * w + xa);
+    const float d = load_sample(f, dtype, base + (int64_t)yc * w + xb);
+    const float top = __fadd_rn(__fmul_rn(op.omx, a), __fmul_rn(op.fx, b));
+    const float bot = __fadd_rn(__fmul_rn(op.omx, c), __fmul_rn(op.fx, d));
+    return __fadd_rn(__fmul_rn(op.omy, top), __fmul_rn(op.fy, bot));
+}
+
+__global__ void correct_kernel(const void* __restrict__ frames, int dtype, int64_t n, int h, int w,
+                               const vb_motion* __restrict__ vec, float* __restrict__ out) {
+    const int64_t hw = (int64_t)h * w;
+    for (int64_t t = blockIdx.y; t < n; t += gridDim.y) {
+        const WarpOp op = make_warp(vec, t);
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hw; i += (int64_t)gridDim.x * blockDim.x) {
+            const int y = (int)(i / w), x = (int)(i - (int64_t)y * w);
+            out[t * hw + i] = warp_sample(frames, dtype, t * hw, h, w, op, y, x);
+        }
+    }
+}
+
+int launch_correct(const void* frames, int dtype, int64_t n, int h, int w, const vb_motion* vec, float* out,
+                   cudaStream_t s) {
+    if (n <= 0) return VB_OK;
+    const int64_t hw = (int64_t)h * w;
+    dim3 grid((unsigned)std::min<int64_t>((hw + 255) / 256, 64), (unsigned)std::min<int64_t>(n, 65535));
+    correct_kernel<<<grid, 256, 0, s>>>(frames, dtype, n, h, w, vec, out);
+    VB_LAUNCHED();
+    return VB_OK;
+}
+
+// ------------------------------------------------------------------ K3
+constexpr int kTY = 32, kTX = 64, kK3Threads = 256;
+constexpr int kMaxWR = 16;
+constexpr int kPix = kTY * kTX / kK3Threads;  // pixels owned per thread
+
+struct Weights {
+    double w[2 * kMaxWR + 1];  // centre at index wr (scipy weights reversed == same, symmetric)
+};
+
+struct K3Args {
+    const void* frames;
+    int dtype;
+    const vb_motion* vec;  // may be null: frames are already corrected
+    int64_t n;             // frames in this launch (from the first block start)
+    int h, w, L, wr;
+    Weights wt;
+    float* corrected;  // may be null
+    float* spatial;    // [blocks][h][w]
+    float* smoothed;   // [n][h][w] (time-major, block frames contiguous)
+};
+
+// scipy correlate1d symmetric kernel: o = x0*w0; for j=-r..-1: o += (x[j]+x[-j])*w[j]
+__device__ __forceinline__ double corr_sym(const float* line, int stride, const double* wc, int r) {
+    double o = __dmul_rn((double)line[0], wc[0]);
+    for (int j = -r; j < 0; ++j) {
+        const double pr = __dadd_rn((double)line[j * stride], (double)line[-j * stride]);
+        o = __dadd_rn(o, __dmul_rn(pr, wc[j]));
+    }
+    return o;
+}
+
+__global__ void __launch_bounds__(kK3Threads) warp_smooth_kernel(K3Args a) {
+    extern __shared__ __align__(16) float sm3[];
+    const int wr = a.wr;
+    const int EH = kTY + 2 * wr, EW = kTX + 2 * wr;
+    const int EWP = EW | 1;
+    float* sC = sm3;             // [EH][EWP]   corrected tile + halo
+    float* sV = sm3 + EH * EWP;  // [kTY][EWP]  after the H (vertical) pass
+    __shared__ double s_w[2 * kMaxWR + 1];
+    const int tid = threadIdx.x;
+    if (tid < 2 * wr + 1) s_w[tid] = a.wt.w[tid];
+
+    const int ty0 = blockIdx.y * kTY, tx0 = blockIdx.x * kTX;
+    const int blk = blockIdx.z;
+    const int64_t t0 = (int64_t)blk * a.L;
+    const int64_t t1 = (t0 + a.L < a.n ? t0 + a.L : a.n);
+    const int64_t hw = (int64_t)a.h * a.w;
+    const int lx = tid % kTX, ly0 = tid / kTX;  // owned pixels: (ly0 + 4k, lx)
+    double sum[kPix];
+#pragma unroll
+    for (int k = 0; k < kPix; ++k) sum[k] = 0.0;
+    __syncthreads();
+    const double* wc = s_w + wr;
+
+    for (int64_t t = t0; t < t1; ++t) {
+        const WarpOp op = make_warp(a.vec, t);
+        // 1. corrected frame on the tile + reflect halo
+        for (int i = tid; i < EH * EW; i += kK3Threads) {
+            const int ey = i / EW, ex = i - ey * EW;
+            const int gy = reflect_index(ty0 - wr + ey, a.h), gx = reflect_index(tx0 - wr + ex, a.w);
+            sC[ey * EWP + ex] = warp_sample(a.frames, a.dtype, t * hw, a.h, a.w, op, gy, gx);
+        }
+        __syncthreads();
+        // 2. own pixels: spatial sum + corrected output; then the H pass
+#pragma unroll
+        for (int k = 0; k < kPix; ++k) {
+            const int ly = ly0 + 4 * k, gy = ty0 + ly, gx = tx0 + lx;
+            const float c = sC[(ly + wr) * EWP + lx + wr];
+            sum[k] += (double)c;
+            if (a.corrected && gy < a.h && gx < a.w) a.corrected[t * hw + (int64_t)gy * a.w + gx] = c;
+        }
+        for (int i = tid; i < kTY * EW; i += kK3Threads) {
+            const int r = i / EW, c = i - r * EW;
+            sV[r * EWP + c] = (float)corr_sym(sC + (r + wr) * EWP + c, EWP, wc, wr);
+        }
+        __syncthreads();
+        // 3. W pass on own pixels -> smoothed (time-major)
+#pragma unroll
+        for (int k = 0; k < kPix; ++k) {
+            const int ly = ly0 + 4 * k, gy = ty0 + ly, gx = tx0 + lx;
+            const float sv = (float)corr_sym(sV + ly * EWP + lx + wr, 1, wc, wr);
+            if (gy < a.h && gx < a.w) a.smoothed[t * hw + (int64_t)gy * a.w + gx] = sv;
+        }
+    }
+    if (!a.spatial) return;
+    const double nblk = (double)(t1 - t0);
+#pragma unroll
+    for (int k = 0; k < kPix; ++k) {
+        const int gy = ty0 + ly0 + 4 * k, gx = tx0 + lx;
+        if (gy < a.h && gx < a.w) a.spatial[(int64_t)blk * hw + (int64_t)gy * a.w + gx] = (float)(sum[k] / nblk);
+    }
+}
+
+// ------------------------------------------------------------------ K4
+constexpr int kK4Pix = 16, kK4Threads = 128;
+
+// k-th smallest (0-based) of the warp's values (uint32 patterns of
+// non-negative floats; padding = 0xffffffff never counts).
+template <int VPL>
+__device__ __forceinline__ uint32_t warp_select(const uint32_t (&v)[VPL], uint32_t lo, uint32_t hi, int k) {
+    const uint32_t diff = lo ^ hi;
+    if (diff == 0) return lo;
+    const int nb = 32 - __clz(diff);
+    uint32_t ans = lo & ~((nb == 32) ? 0xffffffffu : ((1u << nb) - 1u));
+    for (int b = nb - 1; b >= 0; --b) {
+        const uint32_t cand = ans | (1u << b);
+        uint32_t c = 0;
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) c += v[i] < cand ? 1u : 0u;
+        c = __reduce_add_sync(0xffffffffu, c);
+        if ((int)c <= k) ans = cand;
+    }
+    return ans;
+}
+
+template <int VPL>
+__global__ void __launch_bounds__(kK4Threads) median_kernel(const float* __restrict__ smoothed, int64_t n,
+                                                             int64_t hw, int L, float* __restrict__ temporal) {
+    extern __shared__ float sm4[];  // [L][kK4Pix + 1]
+    const int blk = blockIdx.y;
+    const int64_t t0 = (int64_t)blk * L;
+    const int cnt = (int)((int64_t)L < n - t0 ? (int64_t)L : n - t0);
+    const int64_t p0 = (int64_t)blockIdx.x * kK4Pix;
+    const int np = (int)((int64_t)kK4Pix < hw - p0 ? (int64_t)kK4Pix : hw - p0);
+    for (int i = threadIdx.x; i < cnt * kK4Pix; i += kK4Threads) {
+        const int tt = i / kK4Pix, pp = i - tt * kK4Pix;
+        sm4[tt * (kK4Pix + 1) + pp] = pp < np ? __ldcs(smoothed + (t0 + tt) * hw + p0 + pp) : 0.f;
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mid = cnt / 2;
+    for (int pp = warp; pp < np; pp += kK4Threads / 32) {
+        uint32_t v[VPL];
+        uint32_t lo = 0xffffffffu, hi = 0u;
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+            const int tt = lane + 32 * i;
+            v[i] = tt < cnt ? __float_as_uint(sm4[tt * (kK4Pix + 1) + pp]) : 0xffffffffu;
+            if (tt < cnt) {
+                lo = min(lo, v[i]);
+                hi = max(hi, v[i]);
+            }
+        }
+        lo = __reduce_min_sync(0xffffffffu, lo);
+        hi = __reduce_max_sync(0xffffffffu, hi);
+        float med;
+        if (cnt & 1) {
+            med = __uint_as_float(warp_select<VPL>(v, lo, hi, mid));
+        } else {
+            const uint32_t a = warp_select<VPL>(v, lo, hi, mid - 1);
+            uint32_t le = 0, above = 0xffffffffu;
+#pragma unroll
+            for (int i = 0; i < VPL; ++i) {
+                le += v[i] <= a ? 1u : 0u;
+                if (v[i] > a) above = min(above, v[i]);
+            }
+            le = __reduce_add_sync(0xffffffffu, le);
+            above = __reduce_min_sync(0xffffffffu, above);
+            const uint32_t b = ((int)le >= mid + 1) ? a : above;
+            med = __fmul_rn(__fadd_rn(__uint_as_float(a), __uint_as_float(b)), 0.5f);
+        }
+        if (lane == 0) temporal[(int64_t)blk * hw + p0 + pp] = __fsub_rn(__uint_as_float(hi), med);
+    }
+}
+
+// Fallback for blocks longer than 1024 frames: the column is re-read from
+// global memory (L2) on each bisection step.
+__global__ void median_kernel_long(const float* __restrict__ smoothed, int64_t n, int64_t hw, int L,
+                                   float* __restrict__ temporal) {
+    const int blk = blockIdx.y;
+    const int64_t t0 = (int64_t)blk * L;
+    const int cnt = (int)((int64_t)L < n - t0 ? (int64_t)L : n - t0);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t p = (int64_t)blockIdx.x * (blockDim.x / 32) + warp;
+    if (p >= hw) return;
+    const float* col = smoothed + t0 * hw + p;
+    uint32_t lo = 0xffffffffu, hi = 0;
+    for (int tt = lane; tt < cnt; tt += 32) {
+        const uint32_t u = __float_as_uint(col[(int64_t)tt * hw]);
+        lo = min(lo, u);
+        hi = max(hi, u);
+    }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    auto select = [&](int k) -> uint32_t {
+        const uint32_t diff = lo ^ hi;
+        if (diff == 0) return lo;
+        const int nb = 32 - __clz(diff);
+        uint32_t ans = lo & ~((nb == 32) ? 0xffffffffu : ((1u << nb) - 1u));
+        for (int b = nb - 1; b >= 0; --b) {
+            const uint32_t cand = ans | (1u << b);
+            uint32_t c = 0;
+            for (int tt = lane; tt < cnt; tt += 32) c += __float_as_uint(col[(int64_t)tt * hw]) < cand ? 1u : 0u;
+            c = __reduce_add_sync(0xffffffffu, c);
+            if ((int)c <= k) ans = cand;
+        }
+        return ans;
+    };
+    const int mid = cnt / 2;
+    float med;
+    if (cnt & 1) {
+        med = __uint_as_float(select(mid));
+    } else {
+        const uint32_t a = select(mid - 1);
+        uint32_t le = 0, above = 0xffffffffu;
+        for (int tt = lane; tt < cnt; tt += 32) {
+            const uint32_t u = __float_as_uint(col[(int64_t)tt * hw]);
+            le += u <= a ? 1u : 0u;
+            if (u > a) above = min(above, u);
+        }
+        le = __reduce_add_sync(0xffffffffu, le);
+        above = __reduce_min_sync(0xffffffffu, above);
+        const uint32_t b = ((int)le >= mid + 1) ? a : above;
+        med = __fmul_rn(__fadd_rn(__uint_as_float(a), __uint_as_float(b)), 0.5f);
+    }
+    if (lane == 0) temporal[(int64_t)blk * hw + p] = __fsub_rn(__uint_as_float(hi), med);
+}
+
+template <int VPL>
+static int launch_median_vpl(const float* sm, int64_t n, int64_t hw, int L, int nblk, float* temporal,
+                             cudaStream_t s) {
+    const size_t smem = (size_t)L * (kK4Pix + 1) * sizeof(float);
+    VB_CUDA(cudaFuncSetAttribute(median_kernel<VPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid((unsigned)((hw + kK4Pix - 1) / kK4Pix), (unsigned)nblk);
+    median_kernel<VPL><<<grid, kK4Threads, smem, s>>>(sm, n, hw, L, temporal);
+    VB_LAUNCHED();
+    return VB_OK;
+}
+
+static int launch_median(const float* sm, int64_t n, int64_t hw, int L, int nblk, float* temporal, cudaStream_t s) {
+    const int vpl = (L + 31) / 32;
+    if (vpl <= 1) return launch_median_vpl<1>(sm, n, hw, L, nblk, temporal, s);
+    if (vpl <= 2) return launch_median_vpl<2>(sm, n, hw, L, nblk, temporal, s);
+    if (vpl <= 4) return launch_median_vpl<4>(sm, n, hw, L, nblk, temporal, s);
+    if (vpl <= 8) return launch_median_vpl<8>(sm, n, hw, L, nblk, temporal, s);
+    if (vpl <= 16) return launch_median_vpl<16>(sm, n, hw, L, nblk, temporal, s);
+    if (vpl <= 32) return launch_median_vpl<32>(sm, n, hw, L, nblk, temporal, s);
+    dim3 grid((unsigned)((hw + 3) / 4), (unsigned)nblk);
+    median_kernel_long<<<grid, 128, 0, s>>>(sm, n, hw, L, temporal);
+    VB_LAUNCHED();
+    return VB_OK;
+}
+
+int launch_summarize(const void* frames, int dtype, const vb_motion* vec, int64_t n, int h, int w, int seg_len,
+                     const double* weights, int wradius, float* corrected, float* spatial, float* temporal,
+                     cudaStream_t s) {
+    if (n <= 0) return VB_OK;
+    if (wradius > kMaxWR) return fail(VB_EINVAL, "smoothing radius too large (max 16)");
+    const int64_t hw = (int64_t)h * w;
+    const int64_t nblk_total = (n + seg_len - 1) / seg_len;
+    // blocks per launch: bound the smoothed scratch to ~4 GB
+    const size_t blk_bytes = (size_t)seg_len * hw * sizeof(float);
+    int64_t per = std::max<int64_t>(1, (int64_t)((size_t)4 << 30) / (int64_t)blk_bytes);
+    per = std::min(per, nblk_total);
+    float* smoothed = nullptr;
+    VB_CUDA(cudaMallocAsync(&smoothed, blk_bytes * per, s));
+    K3Args a;
+    a.dtype = dtype;
+    a.h = h;
+    a.w = w;
+    a.L = seg_len;
+    a.wr = wradius;
+    for (int i = 0; i < 2 * wradius + 1; ++i) a.wt.w[i] = weights[i];
+    const int EH = kTY + 2 * wradius, EWP = (kTX + 2 * wradius) | 1;
+    const size_t smem3 = (size_t)(EH + kTY) * EWP * sizeof(float);
+    cudaError_t e = cudaFuncSetAttribute(warp_smooth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
+    int rc = e == cudaSuccess ? VB_OK : cuda_fail(e, "cudaFuncSetAttribute(warp_smooth_kernel)");
+    const size_t esz = dtype == VB_U16 ? 2 : 4;
+    for (int64_t b0 = 0; b0 < nblk_total && rc == VB_OK; b0 += per) {
+        const int nb = (int)std::min(per, nblk_total - b0);
+        const int64_t f0 = b0 * seg_len;
+        const int64_t nf = std::min<int64_t>((int64_t)nb * seg_len, n - f0);
+        a.frames = (const char*)frames + (size_t)f0 * hw * esz;
+        a.vec = vec ? vec + f0 : nullptr;
+        a.n = nf;
+        a.corrected = corrected ? corrected + (size_t)f0 * hw : nullptr;
+        a.spatial = spatial + (size_t)b0 * hw;
+        a.smoothed = smoothed;
+        dim3 grid((unsigned)((w + kTX - 1) / kTX), (unsigned)((h + kTY - 1) / kTY), (unsigned)nb);
+        warp_smooth_kernel<<<grid, kK3Threads, smem3, s>>>(a);
+        launches().fetch_add(1, std::memory_order_relaxed);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) { rc = cuda_fail(e, "warp_smooth_kernel"); break; }
+        rc = launch_median(smoothed, nf, hw, seg_len, nb, temporal + (size_t)b0 * hw, s);
+    }
+    cudaFreeAsync(smoothed, s);
+    return rc;
+}
+
+// Smoothing only (scipy gaussian_filter on each frame, summarize.py:60-73):
+// K3 with one-frame blocks, no warp and no spatial summary.
+int launch_smooth(const void* frames, int dtype, int64_t n, int h, int w, const double* weights, int wradius,
+                  float* out, cudaStream_t s) {
+    if (n <= 0) return VB_OK;
+    if (wradius > kMaxWR) return fail(VB_EINVAL, "smoothing radius too large (max 16)");
+    const int64_t hw = (int64_t)h * w;
+    K3Args a;
+    a.dtype = dtype;
+    a.vec = nullptr;
+    a.h = h;
+    a.w = w;
+    a.L = 1;
+    a.wr = wradius;
+    for (int i = 0; i < 2 * wradius + 1; ++i) a.wt.w[i] = weights[i];
+    a.corrected = nullptr;
+    a.spatial = nullptr;
+    const int EH = kTY + 2 * wradius, EWP = (kTX + 2 * wradius) | 1;
+    const size_t smem3 = (size_t)(EH + kTY) * EWP * sizeof(float);
+    VB_CUDA(cudaFuncSetAttribute(warp_smooth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+    const size_t esz = dtype == VB_U16 ? 2 : 4;
+    for (int64_t f0 = 0; f0 < n; f0 += 65535) {
+        const int64_t nf = std::min<int64_t>(65535, n - f0);
+        a.frames = (const char*)frames + (size_t)f0 * hw * esz;
+        a.n = nf;
+        a.smoothed = out + (size_t)f0 * hw;
+        dim3 grid((unsigned)((w + kTX - 1) / kTX), (unsigned)((h + kTY - 1) / kTY), (unsigned)nf);
+        warp_smooth_kernel<<<grid, kK3Threads, smem3, s>>>(a);
+        VB_LAUNCHED();
+    }
+    return VB_OK;
+}
+
+}  // namespace vb

@@ -1,0 +1,92 @@
+// Internal shared declarations for libvoltb200 (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/voltb200.h"
+
+namespace vb {
+
+// ---- error plumbing -------------------------------------------------------
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+std::atomic<int64_t>& launches();
+
+#define VB_CUDA(call)                                               \
+    do {                                                            \
+        cudaError_t e_ = (call);                                    \
+        if (e_ != cudaSuccess) return ::vb::cuda_fail(e_, #call);   \
+    } while (0)
+
+#define VB_LAUNCHED()                                                      \
+    do {                                                                   \
+        ::vb::launches().fetch_add(1, std::memory_order_relaxed);          \
+        cudaError_t e_ = cudaGetLastError();                               \
+        if (e_ != cudaSuccess) return ::vb::cuda_fail(e_, "kernel launch"); \
+    } while (0)
+
+// ---- geometry ---------------------------------------------------------------
+// A patch group is a run of patches with the same origin y whose union window
+// (all candidate offsets) is staged once in shared memory by one CTA.
+struct PatchGroup {
+    int32_t first;  // first patch index (patches of a group are contiguous)
+    int32_t count;  // patches in the group
+    int32_t x0;     // union window left column  (min px - R)
+    int32_t y0;     // union window top row      (py - R)
+    int32_t wu;     // union window width        (max px - min px + P + 2R)
+    int32_t pad[3];
+};
+
+static constexpr int kMaxRadius = 31;  // _native.pyx:63-66 (acc[63])
+static constexpr int kMaxGroup = 32;
+
+// Prepared template for one recording (device memory).
+struct Templates {
+    float* tmpl = nullptr;       // [N][P][TP] centred template patches r - mean_p (f32)
+    double* rvar = nullptr;      // [N] n*variance of each template patch (f64)
+    double* rmean = nullptr;     // [N] template patch means (aliases rvar + N)
+    int32_t* origins = nullptr;  // [N][2] (x, y)
+    int32_t* patch_col = nullptr;// [N] column of the patch's dx=-R window inside its group union
+    PatchGroup* groups = nullptr;// [n_groups]
+    int n = 0, n_groups = 0, tp = 0, max_g = 0, max_wu = 0;
+};
+
+// Kernel entry points implemented in the .cu files (host-side launchers).
+int launch_template_sum(const void* frames, int dtype, int64_t n, int64_t hw, double* sum,
+                        int accumulate, cudaStream_t s);
+int launch_template_finish(const double* sum, int64_t n_total, int64_t hw, float* ref, cudaStream_t s);
+int launch_prep_templates(const float* ref, int h, int w, int patch, const Templates& t, cudaStream_t s);
+int launch_motion(const Templates& t, int h, int w, int patch, int radius, const void* frames, int dtype,
+                  int64_t n_frames, int subpixel, vb_motion* vectors, double* scores, cudaStream_t s);
+int launch_correct(const void* frames, int dtype, int64_t n, int h, int w, const vb_motion* vec,
+                   float* out, cudaStream_t s);
+int launch_summarize(const void* frames, int dtype, const vb_motion* vec, int64_t n, int h, int w,
+                     int seg_len, const double* weights, int wradius, float* corrected, float* spatial,
+                     float* temporal, cudaStream_t s);
+int launch_smooth(const void* frames, int dtype, int64_t n, int h, int w, const double* weights, int wradius,
+                  float* out, cudaStream_t s);
+
+// Device helpers ---------------------------------------------------------------
+__device__ __forceinline__ float load_sample(const void* base, int dtype, int64_t idx) {
+    if (dtype == VB_U16) return (float)__ldg(reinterpret_cast<const uint16_t*>(base) + idx);
+    return __ldg(reinterpret_cast<const float*>(base) + idx);
+}
+
+__host__ __device__ __forceinline__ int clampi(int v, int lo, int hi) {
+    return v < lo ? lo : (v > hi ? hi : v);
+}
+
+// scipy "reflect" boundary (half-sample symmetric), any overhang.
+__host__ __device__ __forceinline__ int reflect_index(int i, int n) {
+    int period = 2 * n;
+    int m = i % period;
+    if (m < 0) m += period;
+    return m >= n ? period - 1 - m : m;
+}
+
+}  // namespace vb

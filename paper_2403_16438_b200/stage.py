@@ -1,0 +1,174 @@
+"""Fused preprocessing stage: correct_motion (motion.py:217-241) followed by
+summarize (summarize.py:99-102), as pipeline.py:198-224 runs them -- on one
+device, without materialising the corrected video unless asked.
+
+Three entry points:
+  * preprocess(video, ...)        -- numpy/Video in, numpy out (API parity).
+  * DevicePreprocessor            -- device-resident recording; the bench's
+                                     `value` path (inputs already in HBM).
+  * HostStage                     -- vb_stage C-ABI executor over a HOST
+                                     buffer: chunked pinned H2D / compute / D2H
+                                     overlap; the bench's `e2e` path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device as D
+from . import _lib
+from . import motion as M
+from .summarize import DEFAULT_SEGMENT_LENGTH, DEFAULT_SMOOTH_SIGMA, SummaryPair, gaussian_weights, summarize_device
+from .video import Video
+
+
+@dataclass
+class StageConfig:
+    patch_size: int = M.DEFAULT_PATCH_SIZE
+    search_radius: int = M.DEFAULT_SEARCH_RADIUS
+    subpixel: bool = True
+    ref_frames: int | None = None  # None -> motion.REFERENCE_FRAMES at call time
+    segment_length: int = DEFAULT_SEGMENT_LENGTH
+    sigma: float = DEFAULT_SMOOTH_SIGMA
+
+
+@dataclass
+class DeviceResult:
+    vectors: torch.Tensor            # device buffer of vb_motion records
+    spatial: torch.Tensor            # [K, H, W] float32
+    temporal: torch.Tensor           # [K, H, W] float32
+    corrected: torch.Tensor | None   # [T, H, W] float32 or None
+    n_frames: int
+
+    def vectors_numpy(self) -> np.ndarray:
+        return D.motion_to_numpy(self.vectors, self.n_frames)
+
+
+class DevicePreprocessor:
+    """Reusable stage for recordings of one geometry already in HBM.
+
+    run(frames) = template (f64 mean of the first M frames) -> template patch
+    prep -> ZNCC motion search for every frame -> fused warp + per-block
+    spatial mean / smoothing / max-minus-median.  5 + 2*ceil(T/B) kernel
+    launches, all on the current stream."""
+
+    def __init__(self, height: int, width: int, config: StageConfig | None = None):
+        self.cfg = config or StageConfig()
+        c = self.cfg
+        if c.search_radius < 1:
+            raise ValueError("search_radius must be >= 1")
+        if c.segment_length < 2:
+            raise ValueError("segment length must be >= 2")
+        self.height, self.width = height, width
+        self.grid = M.PatchGrid.cover(height, width, c.patch_size, margin=c.search_radius)
+        self.plan = M.MotionPlan(height, width, self.grid.origins, c.patch_size, c.search_radius)
+        self.weights, self.wradius = gaussian_weights(c.sigma)
+
+    def run(self, frames: torch.Tensor, corrected_out: torch.Tensor | None = None,
+            vectors_out: torch.Tensor | None = None) -> DeviceResult:
+        t = frames.shape[0]
+        if t % self.cfg.segment_length == 1:
+            raise ValueError("temporal summary needs at least 2 frames")
+        m = M.REFERENCE_FRAMES if self.cfg.ref_frames is None else self.cfg.ref_frames
+        ref = M.device_reference(frames, m)
+        self.plan.set_reference(ref)
+        vec, _ = self.plan.estimate(frames, self.cfg.subpixel, out=vectors_out)
+        sp, tp = summarize_device(frames, self.cfg.segment_length, self.cfg.sigma, vectors_dev=vec,
+                                  corrected_out=corrected_out)
+        return DeviceResult(vec, sp, tp, corrected_out, t)
+
+    def close(self):
+        self.plan.close()
+
+
+def preprocess(video, config: StageConfig | None = None, return_corrected: bool = True):
+    """correct_motion + summarize in one device pass.
+
+    Returns (corrected Video | None, list[MotionVector], list[SummaryPair]) --
+    the same values as the reference's correct_motion(video, MotionConfig(...))
+    followed by summarize(corrected, L, sigma)."""
+    v = Video.wrap(video)
+    dev = D.require_cuda()
+    frames = D.as_device_frames(v.samples, dev)
+    pre = DevicePreprocessor(v.height, v.width, config)
+    try:
+        corr = torch.empty(frames.shape, dtype=torch.float32, device=dev) if return_corrected else None
+        res = pre.run(frames, corrected_out=corr)
+        rec = res.vectors_numpy()
+        sp, tp = res.spatial.cpu().numpy(), res.temporal.cpu().numpy()
+        out = Video(corr.cpu().numpy(), frame_rate=v.frame_rate) if return_corrected else None
+    finally:
+        pre.close()
+    vectors = M._vectors_from_numpy(rec)
+    pairs = [SummaryPair(i, sp[i], tp[i]) for i in range(sp.shape[0])]
+    return out, vectors, pairs
+
+
+class HostStage:
+    """vb_stage: the C-ABI whole-stage executor over host buffers."""
+
+    def __init__(self, height: int, width: int, config: StageConfig | None = None, device: int | None = None,
+                 chunk_frames: int = 0):
+        self.cfg = config or StageConfig()
+        c = self.cfg
+        dev = D.require_cuda() if device is None else torch.device("cuda", device)
+        m = M.REFERENCE_FRAMES if c.ref_frames is None else c.ref_frames
+        sc = _lib.VbStageConfig(height, width, c.patch_size, c.search_radius, int(c.subpixel), m,
+                                c.segment_length, float(c.sigma), dev.index or 0, int(chunk_frames))
+        h = C.c_void_p()
+        _lib.call("vb_stage_create", C.byref(h), C.byref(sc))
+        self._h = h
+        w, r = gaussian_weights(c.sigma)
+        self._w = w
+        _lib.call("vb_stage_set_weights", self._h, w.ctypes.data, r)
+        self.height, self.width = height, width
+
+    def run(self, frames: np.ndarray, corrected: bool = False):
+        """frames: uint16/float32 (T,H,W) host array (pinned or pageable).
+        Returns (vectors record array, spatial [K,H,W], temporal [K,H,W], corrected|None)."""
+        a = frames
+        if isinstance(a, torch.Tensor):
+            assert not a.is_cuda
+            dtype = D.vb_dtype(a)
+            ptr, t = a.data_ptr(), a.shape[0]
+        else:
+            a = np.ascontiguousarray(a)
+            if a.dtype not in (np.uint16, np.float32):
+                a = a.astype(np.float32)
+            dtype = _lib.VB_U16 if a.dtype == np.uint16 else _lib.VB_F32
+            ptr, t = a.ctypes.data, a.shape[0]
+        k = math.ceil(t / self.cfg.segment_length)
+        vec = np.empty(t, dtype=_lib.MOTION_DTYPE)
+        sp = np.empty((k, self.height, self.width), np.float32)
+        tp = np.empty((k, self.height, self.width), np.float32)
+        corr = np.empty((t, self.height, self.width), np.float32) if corrected else None
+        self.run_into(ptr, dtype, t, vec, sp, tp, corr)
+        return vec, sp, tp, corr
+
+    def run_into(self, frames_ptr: int, dtype: int, t: int, vec, sp, tp, corr=None) -> None:
+        """Zero-allocation variant: all outputs are caller-provided host buffers
+        (numpy arrays or pinned torch tensors)."""
+        def p(x):
+            if x is None:
+                return None
+            return x.data_ptr() if isinstance(x, torch.Tensor) else x.ctypes.data
+        _lib.call("vb_stage_run_host", self._h, frames_ptr, dtype, t, p(vec), p(sp), p(tp), p(corr))
+
+    @property
+    def last_launches(self) -> int:
+        return int(_lib.load().vb_stage_last_launches(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None) is not None:
+            _lib.load().vb_stage_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
