@@ -1,0 +1,429 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 preprocessing stage (motion correction -> per-block
+summary images) on BASELINE.json's paper-scale workload (configs[1], "c2":
+10,000 x 256 x 512 uint16 frames, search radius 8, patch 21, L = 1000, M = 100).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = the whole stage over one rank's 10,000-frame recording shard:
+template (f64 mean of the recording's first M frames; all-reduced over NCCL
+when N > 1) -> ZNCC motion search for every frame -> fused warp + per-block
+spatial mean / smoothing / max-minus-median, corrected video written to HBM.
+`value` = frames processed by all ranks / max-over-ranks device time (inputs
+resident in HBM, CUDA events).  `e2e` = the same through the C-ABI host entry
+point vb_stage_run_host with pinned host input (H2D of every frame, D2H of
+vectors + summaries inside the timed region).  Under torchrun each rank
+takes its own shard (weak scaling).  `--impl reference` times the unmodified
+reference (voltseg, oracle/_ref) on the host CPU cores on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "frames/sec of preprocessing stage at 1/2/4/8 B200 (+% HBM roofline) vs CPU ref"
+UNIT = "frames/s"
+CONFIG = "c2"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", default=CONFIG)
+    p.add_argument("--frames", type=int, default=0, help="override frames per rank (profiling only)")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-corrected", action="store_true", help="do not materialise the corrected video")
+    p.add_argument("--cpu-sample", type=int, default=1000, help="frames in the CPU baseline sample")
+    p.add_argument("--ref-step-frames", type=int, default=400, help="frames per --impl reference step")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- workload
+def workload(cfg_name: str, frames_override: int):
+    from paper_2403_16438_b200 import synth
+
+    cfg = synth.CONFIGS[cfg_name]
+    if frames_override:
+        cfg = cfg.with_frames(frames_override)
+    return cfg
+
+
+def algorithmic_numbers(cfg, n_patches: int):
+    """bytes/frame = H*W*(2 u16 read + 4 f32 corrected write) + 8*H*W/L;
+    ZNCC cross-term flops/frame = 2 * N_patch * (2r+1)^2 * P^2."""
+    hw = cfg.height * cfg.width
+    bytes_frame = hw * (2 + 4) + 8 * hw / cfg.segment_length
+    flops_frame = 2.0 * n_patches * (2 * cfg.radius + 1) ** 2 * 21 * 21
+    return bytes_frame, flops_frame
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()), "MEASURED_PEAKS.json"
+        except ValueError:
+            pass
+    return {"hbm_gbs": 6650.0}, "fallback B200_PROFILING.md"
+
+
+# ---------------------------------------------------------------- CPU reference
+def reference_stage_fps(frames_f32: np.ndarray, cfg, threads: int):
+    """Time the UNMODIFIED reference stage (voltseg native backend) on host cores:
+    correct_motion(video, MotionConfig(search_radius=r, threads=N)) then
+    summarize(corrected, L, 3.0) -- BASELINE.md section 3."""
+    from oracle import ref
+
+    motion, summarize, kernels, video_io = ref.load()
+    motion.REFERENCE_FRAMES = cfg.ref_frames  # read at call time (motion.py:213)
+    video = video_io.Video(frames_f32, frame_rate=cfg.fps)
+    t0 = time.perf_counter()
+    corrected, _vecs = motion.correct_motion(video, motion.MotionConfig(search_radius=cfg.radius, threads=threads))
+    summarize.summarize(corrected, cfg.segment_length, 3.0)
+    dt = time.perf_counter() - t0
+    return frames_f32.shape[0] / dt, dt, kernels.BACKEND
+
+
+def oracle_port_fps(frames_f32: np.ndarray, cfg, threads: int):
+    from oracle import oracle as O
+
+    t0 = time.perf_counter()
+    O.preprocess(frames_f32, 21, cfg.radius, True, cfg.ref_frames, cfg.segment_length, 3.0, threads,
+                 want_corrected=False)
+    dt = time.perf_counter() - t0
+    return frames_f32.shape[0] / dt, dt
+
+
+def host_sample(cfg, n: int) -> np.ndarray:
+    """The first n frames of the (rank 0) recording, as the reference's float32 Video data."""
+    import torch
+
+    from paper_2403_16438_b200 import synth
+
+    if torch.cuda.is_available():
+        v = synth.generate(cfg, "cuda")[:n]
+        arr = v.view(torch.int16).cpu().numpy().view(np.uint16)
+        del v
+        torch.cuda.empty_cache()
+    else:
+        arr = synth.generate_numpy(cfg.with_frames(n))
+    return arr.astype(np.float32)
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    cfg = workload(args.config, args.frames)
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    n = min(args.ref_step_frames, cfg.frames)
+    frames = host_sample(cfg, n)
+    kind = "reference"
+    try:
+        from oracle import ref as _r
+
+        if not _r.available():
+            raise RuntimeError("oracle/_ref missing")
+        step = lambda: reference_stage_fps(frames, cfg, threads)[1]  # noqa: E731
+    except Exception:  # reference not built: oracle port (C restatement)
+        kind = "port"
+        step = lambda: oracle_port_fps(frames, cfg, threads)[1]  # noqa: E731
+    for _ in range(args.warmup):
+        step()
+    times = [step() for _ in range(args.steps)]
+    total = sum(times)
+    fps = n * args.steps / total
+    line = {
+        "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic (repo generator, seed 1002)",
+        "impl": "reference",
+        "config": {"workload": f"{cfg.name}: {cfg.frames}x{cfg.height}x{cfg.width} uint16 (step sample: first {n} frames), "
+                               f"r={cfg.radius}, patch=21, L={cfg.segment_length}, M={cfg.ref_frames}",
+                   "threads": threads},
+        "cpu_baseline": {"value": fps, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"first {n} frames of {cfg.name} per step; voltseg correct_motion(threads={threads}) "
+                                   f"+ summarize(L={cfg.segment_length})"},
+        "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2403_16438_b200 import _lib, distributed, stage, synth
+    from paper_2403_16438_b200 import _device as D
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = workload(args.config, args.frames)
+    L = _lib.load()
+    scfg = stage.StageConfig(patch_size=21, search_radius=cfg.radius, subpixel=True, ref_frames=cfg.ref_frames,
+                             segment_length=cfg.segment_length, sigma=3.0)
+    # weak scaling: rank r owns frames [r*T, (r+1)*T) of an N*T-frame recording
+    frames = synth.generate(synth.SynthConfig(**{**cfg.__dict__, "seed": cfg.seed + rank}), dev)
+    t = frames.shape[0]
+    shard = distributed.shard_plan(t * world, cfg.segment_length, world, rank)
+    assert shard.frames == t
+    runner = distributed.ShardedPreprocessor(cfg.height, cfg.width, scfg)
+    corr = None if args.no_corrected else torch.empty((t, cfg.height, cfg.width), dtype=torch.float32, device=dev)
+    torch.cuda.synchronize()
+
+    def step():
+        return runner.run(frames, shard, cfg.ref_frames, corrected_out=corr)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    L.vb_prof_enable(1)
+    launches0 = _lib.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0.record()
+    for _ in range(args.steps):
+        res = step()
+    ev1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = _lib.launch_count() - launches0
+    ms = np.zeros(5, np.float64)
+    cnt = np.zeros(5, np.int64)
+    _lib.check(L.vb_prof_collect(ms.ctypes.data, cnt.ctypes.data, 5))
+    L.vb_prof_enable(0)
+    clk = clocks.stop()
+    elapsed = ev0.elapsed_time(ev1)  # ms, K steps
+    t_max = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    elapsed = float(t_max.item())
+    value = t * world * args.steps / (elapsed / 1e3)
+
+    # sanity: the stage produced finite, non-negative summaries
+    vec = res.vectors_numpy()
+    ok = bool(np.isfinite(res.temporal.float().cpu().numpy()).all() and (res.temporal.min().item() >= 0)
+              and (np.abs(vec["dx"]) <= cfg.radius).all())
+
+    # ---- roofline of the dominant kernel (ZNCC search), CUDA events on its stream ----
+    peaks, peaks_src = measured_peaks()
+    n_patches = runner.pre.plan.n_patches
+    bytes_frame, flops_frame = algorithmic_numbers(cfg, n_patches)
+    zncc_launches = int(cnt[0])
+    zncc_ms = ms[0] / max(zncc_launches, 1)
+    frames_per_launch = t * args.steps / max(zncc_launches, 1)
+    achieved = flops_frame * frames_per_launch / (zncc_ms / 1e3) / 1e12
+    p2 = _lib.C.c_double()
+    p1 = _lib.C.c_double()
+    _lib.check(L.vb_fp32_peak_probe(_lib.C.byref(p2), _lib.C.byref(p1)))
+    fp32_peak = max(p2.value, p1.value)
+    step_ms = elapsed / args.steps
+    kernel_ms_per_step = {n: float(ms[i] / args.steps) for i, n in
+                          enumerate(["zncc_group", "finalize", "warp_smooth", "median", "other"])}
+    hbm_stage = bytes_frame * t / (step_ms / 1e3) / 1e9
+    roofline = {
+        "bound": "fp32", "kernel": "zncc_group_kernel<21,17>",
+        "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
+        "traffic": None,
+        "peak_source": "measured live: FFMA2 (fma.rn.f32x2) probe, vb_fp32_peak_probe",
+        "peak_ffma_scalar": p1.value,
+        "algorithmic": f"{flops_frame:.4g} flop/frame = 2*N_patch({n_patches})*(2r+1)^2*21^2; "
+                       f"{frames_per_launch:.0f} frames/launch; avg launch {zncc_ms:.3f} ms",
+        "kernel_share_of_step": float(ms[0] / args.steps / step_ms),
+        "kernel_ms_per_step": kernel_ms_per_step,
+        "hbm": {"achieved_gbs": hbm_stage, "peak_gbs": peaks.get("hbm_gbs"), "frac": hbm_stage / peaks.get("hbm_gbs", 6552.3),
+                "peak_source": peaks_src,
+                "algorithmic": f"{bytes_frame:.0f} B/frame = H*W*(2+4) + 8*H*W/L (stage, whole step)"},
+    }
+
+    # ---- e2e through the C-ABI host entry point ----
+    e2e = None
+    if not args.no_e2e:
+        host = frames.view(torch.int16).cpu().pin_memory()
+        hs = stage.HostStage(cfg.height, cfg.width, scfg, device=local)
+        k = math.ceil(t / cfg.segment_length)
+        vec_h = np.empty(t, dtype=_lib.MOTION_DTYPE)
+        sp_h = np.empty((k, cfg.height, cfg.width), np.float32)
+        tp_h = np.empty((k, cfg.height, cfg.width), np.float32)
+        m = cfg.ref_frames
+
+        def e2e_step():
+            if world > 1:
+                # the recording's template: rank 0 uploads its first M frames, NCCL all-reduce
+                ts = torch.zeros((cfg.height, cfg.width), dtype=torch.float64, device=dev)
+                if rank == 0:
+                    head = host[:m].to(dev, non_blocking=True).view(torch.uint16)
+                    _lib.call("vb_template_sum", head.data_ptr(), _lib.VB_U16, m, cfg.height, cfg.width,
+                              ts.data_ptr(), 0, D.stream_handle())
+                distributed.allreduce_sum_(ts)
+                ref = torch.empty((cfg.height, cfg.width), dtype=torch.float32, device=dev)
+                _lib.call("vb_template_finish", ts.data_ptr(), m, cfg.height * cfg.width, ref.data_ptr(),
+                          D.stream_handle())
+                torch.cuda.synchronize()
+                _lib.call("vb_stage_set_reference", hs._h, ref.data_ptr())
+            hs.run_into(host.data_ptr(), _lib.VB_U16, t, vec_h, sp_h, tp_h, None, corrected_dev=corr)
+
+        for _ in range(max(args.warmup, 1)):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        w0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        w1 = time.perf_counter()
+        et = torch.tensor([w1 - w0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e_fps = t * world * args.steps / float(et.item())
+        h2d = (t + m) * cfg.height * cfg.width * 2  # rank 0: recording + template head (phase A / all-reduce)
+        d2h = t * 32 + 2 * k * cfg.height * cfg.width * 4
+        e2e = {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "path": "vb_stage_run_host (C ABI), pinned uint16 host input, vectors+summaries to host, "
+                       "corrected video kept in HBM"}
+        hs.close()
+        del host
+
+    # ---- CPU baseline: the reference on this host's cores (rank 0, N=1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n = min(args.cpu_sample, t)
+        sample = frames[:n].view(torch.int16).cpu().numpy().view(np.uint16).astype(np.float32)
+        threads = os.cpu_count() or 1
+        try:
+            fps_ref, dt, backend = reference_stage_fps(sample, cfg, threads)
+            cpu = {"value": fps_ref, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"first {n} frames of {cfg.name} ({dt:.1f} s): voltseg ({backend} backend) "
+                             f"correct_motion(threads={threads}) + summarize(L={cfg.segment_length})"}
+        except Exception as exc:  # noqa: BLE001
+            fps_ref, dt = oracle_port_fps(sample, cfg, threads)
+            cpu = {"value": fps_ref, "unit": UNIT, "cores": threads, "kind": "port",
+                   "sample": f"first {n} frames of {cfg.name} ({dt:.1f} s), oracle C port; reference failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32/f64",
+            "data": f"synthetic (paper_2403_16438_b200.synth, BASELINE.json configs[1], seed {cfg.seed}+rank)",
+            "config": {"workload": f"{cfg.name}: {t}x{cfg.height}x{cfg.width} uint16 per rank, r={cfg.radius}, "
+                                   f"patch=21, L={cfg.segment_length}, M={cfg.ref_frames}, sigma=3",
+                       "per_rank_frames": t, "parallelism": f"time-sharded x{world} (template all-reduce)",
+                       "corrected_video": "written to HBM" if corr is not None else "not materialised",
+                       "l2": "inputs (%.1f GB u16) larger than L2 (126 MB); no flush" % (t * cfg.height * cfg.width * 2 / 1e9)},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "outputs_sane": ok,
+        }
+        print(json.dumps(line), flush=True)
+    runner.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -139,17 +139,37 @@ int vb_stage_create(vb_stage** stage, const vb_stage_config* cfg);
 int vb_stage_set_weights(vb_stage* stage, const double* weights, int wradius);
 /* Runs correct_motion + summarize over a host recording (pinned or pageable).
  * frames_host: dtype [n][h][w]; vectors_host: [n]; spatial/temporal_host:
- * float32 [ceil(n/L)][h][w]; corrected_host: float32 [n][h][w] or NULL (the
- * corrected video then stays on the device only). */
+ * float32 [ceil(n/L)][h][w]; corrected_host: float32 [n][h][w] or NULL;
+ * corrected_dev: device float32 [n][h][w] that receives the whole corrected
+ * video in HBM, or NULL.  With both NULL the corrected frames are only formed
+ * on the fly inside the fused warp/summary kernel. */
 int vb_stage_run_host(vb_stage* stage, const void* frames_host, int dtype, int64_t n_frames,
                       vb_motion* vectors_host, float* spatial_host, float* temporal_host,
-                      float* corrected_host);
+                      float* corrected_host, float* corrected_dev);
 /* Number of device kernels the last vb_stage_run_host launched. */
 int64_t vb_stage_last_launches(const vb_stage* stage);
 int vb_stage_destroy(vb_stage* stage);
 
+/* Use an externally built template (e.g. all-reduced across ranks) for the
+ * following runs instead of averaging the first ref_frames frames of the
+ * input (phase A).  ref_dev: device float32 [h][w], copied; NULL restores the
+ * default. */
+int vb_stage_set_reference(vb_stage* stage, const float* ref_dev);
+
 /* Kernel launches issued by this library since load (all entry points). */
 int64_t vb_launch_count(void);
+
+/* ---------------- measurement hooks (bench.py) ---------------- */
+/* Per-kernel CUDA-event timing on the launching stream: ids 0 zncc search,
+ * 1 finalize (argmax/fit), 2 fused warp+smooth, 3 median, 4 other.
+ * vb_prof_enable(1) clears and starts recording; vb_prof_collect synchronises
+ * the recorded events and returns total ms and launch counts per id. */
+int vb_prof_enable(int on);
+int vb_prof_collect(double* ms, int64_t* counts, int n_ids);
+/* Measured FP32 throughput of this GPU (TFLOP/s) with packed FFMA2
+ * (fma.rn.f32x2) and scalar FFMA dependency chains: the denominator of the
+ * ZNCC kernel's roofline. */
+int vb_fp32_peak_probe(double* tflops_ffma2, double* tflops_ffma);
 
 #ifdef __cplusplus
 }

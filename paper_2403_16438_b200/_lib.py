@@ -55,10 +55,14 @@ SIGNATURES = {
     "vb_smooth_frames": (_i32, [_vp, _i32, _i64, _i32, _i32, _vp, _i32, _vp, _vp]),
     "vb_stage_create": (_i32, [C.POINTER(_vp), C.POINTER(VbStageConfig)]),
     "vb_stage_set_weights": (_i32, [_vp, _vp, _i32]),
-    "vb_stage_run_host": (_i32, [_vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp]),
+    "vb_stage_run_host": (_i32, [_vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _vp]),
     "vb_stage_last_launches": (_i64, [_vp]),
     "vb_stage_destroy": (_i32, [_vp]),
+    "vb_stage_set_reference": (_i32, [_vp, _vp]),
     "vb_launch_count": (_i64, []),
+    "vb_prof_enable": (_i32, [_i32]),
+    "vb_prof_collect": (_i32, [_vp, _vp, _i32]),
+    "vb_fp32_peak_probe": (_i32, [C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }
 
 _lock = threading.Lock()

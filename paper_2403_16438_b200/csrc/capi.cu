@@ -28,6 +28,22 @@ int cuda_fail(cudaError_t e, const char* where) {
 }
 std::atomic<int64_t>& launches() { return g_launches; }
 
+// Scratch (partials, smoothed blocks) comes from the stream-ordered pool;
+// keep freed blocks cached instead of unmapping them at every sync.
+void keep_pool() {
+    static std::atomic<uint64_t> done_mask{0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return;
+    const uint64_t bit = 1ull << dev;
+    if (done_mask.load() & bit) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done_mask.fetch_or(bit);
+}
+
 // motion.py:71-75
 static std::vector<int> positions(int lo, int hi, int stride) {
     std::vector<int> pos;
@@ -143,9 +159,20 @@ int vb_motion_plan_create(vb_motion_plan** out, int height, int width, int patch
     p->origins.assign(origins_host, origins_host + 2 * (size_t)n_origins);
     std::vector<PatchGroup> groups;
     std::vector<int32_t> col;
-    // group width: ~8 patches keeps the CTA at <= ~80 KB of shared memory
-    const int max_g = std::max(1, std::min(kMaxGroup, patch >= 16 ? 8 : 12));
-    build_groups(p->origins, patch, radius, max_g, groups, col);
+    // group width: ~8 patches keeps the CTA at <= ~80 KB of shared memory;
+    // shrink the group until the search CTA fits (large radii)
+    int max_g = std::max(1, std::min(kMaxGroup, patch >= 16 ? 8 : 12));
+    for (;;) {
+        groups.clear();
+        build_groups(p->origins, patch, radius, max_g, groups, col);
+        int mg = 0, mw = 0;
+        for (auto& g : groups) {
+            mg = std::max(mg, (int)g.count);
+            mw = std::max(mw, (int)g.wu);
+        }
+        if (zncc_smem_bytes(patch, radius, mg, mw) <= 160 * 1024 || max_g == 1) break;
+        max_g = std::max(1, max_g / 2);
+    }
     Templates& t = p->t;
     t.n = n_origins;
     t.n_groups = (int)groups.size();

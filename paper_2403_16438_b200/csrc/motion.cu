@@ -433,6 +433,10 @@ static SmemPlan zncc_smem(int P, int R, int tp, int max_g, int max_wu) {
     return sp;
 }
 
+size_t zncc_smem_bytes(int patch, int radius, int max_g, int max_wu) {
+    return zncc_smem(patch, radius, (patch + 3) & ~3, max_g, max_wu).total;
+}
+
 int launch_motion(const Templates& t, int h, int w, int patch, int radius, const void* frames, int dtype,
                   int64_t n_frames, int subpixel, vb_motion* vectors, double* scores, cudaStream_t s) {
     (void)h;
@@ -475,6 +479,7 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     int64_t batch = std::max<int64_t>(1, (int64_t)((256u << 20) / per_frame));
     batch = std::min(batch, n_frames);
     double* partial = nullptr;
+    keep_pool();
     VB_CUDA(cudaMallocAsync(&partial, per_frame * batch, s));
     int rc = VB_OK;
     for (int64_t f0 = 0; f0 < n_frames && rc == VB_OK; f0 += batch) {
@@ -483,13 +488,19 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
         a.n_frames = nb;
         a.partial = partial;
         dim3 grid(t.n_groups, (unsigned)std::min<int64_t>(nb, 65535));
-        fn<<<grid, threads, sp.total, s>>>(a);
+        {
+            ProfScope ps(kProfZncc, s);
+            fn<<<grid, threads, sp.total, s>>>(a);
+        }
         launches().fetch_add(1, std::memory_order_relaxed);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) { rc = cuda_fail(e, "zncc_group_kernel"); break; }
         const int fin_blocks = (int)std::min<int64_t>(nb, 148 * 8);
-        finalize_kernel<<<fin_blocks, 256, SS * sizeof(double), s>>>(
-            partial, t.n_groups, S, t.n, nb, subpixel, vectors + f0, scores ? scores + (size_t)f0 * SS : nullptr);
+        {
+            ProfScope ps(kProfFinalize, s);
+            finalize_kernel<<<fin_blocks, 256, SS * sizeof(double), s>>>(
+                partial, t.n_groups, S, t.n, nb, subpixel, vectors + f0, scores ? scores + (size_t)f0 * SS : nullptr);
+        }
         launches().fetch_add(1, std::memory_order_relaxed);
         e = cudaGetLastError();
         if (e != cudaSuccess) { rc = cuda_fail(e, "finalize_kernel"); break; }

@@ -44,6 +44,7 @@ struct vb_stage {
     float* h_corr[2] = {nullptr, nullptr};
     double* d_tsum = nullptr;
     float* d_ref = nullptr;
+    bool external_ref = false;
     cudaEvent_t ev_h2d[2]{}, ev_comp[2]{}, ev_d2h[2]{};
     int64_t last_launches = 0;
 };
@@ -134,10 +135,23 @@ int vb_stage_set_weights(vb_stage* st, const double* weights, int wradius) {
     return VB_OK;
 }
 
+int vb_stage_set_reference(vb_stage* st, const float* ref_dev) {
+    if (!st) return fail(VB_EINVAL, "null argument");
+    if (!ref_dev) {
+        st->external_ref = false;
+        return VB_OK;
+    }
+    VB_CUDA(cudaSetDevice(st->cfg.device));
+    VB_CUDA(cudaMemcpy(st->d_ref, ref_dev, (size_t)st->cfg.height * st->cfg.width * sizeof(float),
+                       cudaMemcpyDeviceToDevice));
+    st->external_ref = true;
+    return VB_OK;
+}
+
 int64_t vb_stage_last_launches(const vb_stage* st) { return st ? st->last_launches : 0; }
 
 int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t n_frames, vb_motion* vectors_host,
-                      float* spatial_host, float* temporal_host, float* corrected_host) {
+                      float* spatial_host, float* temporal_host, float* corrected_host, float* corrected_dev) {
     if (!st || !frames_host || !vectors_host || !spatial_host || !temporal_host) return fail(VB_EINVAL, "null argument");
     if (dtype != VB_U16 && dtype != VB_F32) return fail(VB_EINVAL, "unsupported sample type");
     const vb_stage_config& c = st->cfg;
@@ -156,7 +170,9 @@ int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t 
     cudaGetLastError();
 
     // (re)allocate the two-slot ring
-    if (st->esz != esz || (corrected_host && !st->d_corr[0]) || (!pinned && !st->h_stage[0])) {
+    const bool ring_corr = corrected_host && !corrected_dev;  // corrected chunks need ring buffers
+    if (st->esz != esz || (ring_corr && !st->d_corr[0]) || (corrected_host && !st->h_corr[0]) ||
+        (!pinned && !st->h_stage[0])) {
         stage_free_buffers(st);
         cudaError_t e = cudaSuccess;
         for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
@@ -164,7 +180,7 @@ int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t 
             e = e ? e : cudaMalloc(&st->d_vec[i], (size_t)C * sizeof(vb_motion));
             e = e ? e : cudaMalloc(&st->d_sp[i], (size_t)cblk * hw * sizeof(float));
             e = e ? e : cudaMalloc(&st->d_tp[i], (size_t)cblk * hw * sizeof(float));
-            if (corrected_host) e = e ? e : cudaMalloc(&st->d_corr[i], (size_t)C * hw * sizeof(float));
+            if (ring_corr) e = e ? e : cudaMalloc(&st->d_corr[i], (size_t)C * hw * sizeof(float));
             e = e ? e : cudaHostAlloc(&st->h_vec[i], (size_t)C * sizeof(vb_motion), cudaHostAllocDefault);
             e = e ? e : cudaHostAlloc(&st->h_sp[i], (size_t)cblk * hw * sizeof(float), cudaHostAllocDefault);
             e = e ? e : cudaHostAlloc(&st->h_tp[i], (size_t)cblk * hw * sizeof(float), cudaHostAllocDefault);
@@ -202,7 +218,7 @@ int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t 
     }
 
     // ---- phase A: template = mean of the first min(n, M) frames ----
-    const int64_t m = std::min<int64_t>(n_frames, c.ref_frames);
+    const int64_t m = st->external_ref ? 0 : std::min<int64_t>(n_frames, c.ref_frames);
     int rc = VB_OK;
     for (int64_t f0 = 0, k = 0; f0 < m && rc == VB_OK; f0 += C, ++k) {
         const int slot = (int)(k & 1);
@@ -214,7 +230,7 @@ int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t 
         if (rc) break;
         VB_CUDA(cudaEventRecord(st->ev_comp[slot], st->s_comp));
     }
-    if (rc == VB_OK) rc = launch_template_finish(st->d_tsum, m, (int64_t)hw, st->d_ref, st->s_comp);
+    if (rc == VB_OK && !st->external_ref) rc = launch_template_finish(st->d_tsum, m, (int64_t)hw, st->d_ref, st->s_comp);
     if (rc == VB_OK) rc = vb_motion_plan_set_reference(st->plan, st->d_ref, st->s_comp);
     for (int i = 0; i < 2 && rc == VB_OK; ++i) VB_CUDA(cudaEventRecord(st->ev_comp[i], st->s_comp));
 
@@ -243,9 +259,9 @@ int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t 
         rc = vb_motion_estimate(st->plan, st->d_frames[slot], dtype, nf, c.subpixel, st->d_vec[slot], nullptr,
                                 st->s_comp);
         if (rc) break;
+        float* corr = corrected_dev ? corrected_dev + (size_t)f0 * hw : (corrected_host ? st->d_corr[slot] : nullptr);
         rc = launch_summarize(st->d_frames[slot], dtype, st->d_vec[slot], nf, c.height, c.width, L,
-                              st->weights.data(), st->wradius, corrected_host ? st->d_corr[slot] : nullptr,
-                              st->d_sp[slot], st->d_tp[slot], st->s_comp);
+                              st->weights.data(), st->wradius, corr, st->d_sp[slot], st->d_tp[slot], st->s_comp);
         if (rc) break;
         VB_CUDA(cudaEventRecord(st->ev_comp[slot], st->s_comp));
         VB_CUDA(cudaStreamWaitEvent(st->s_d2h, st->ev_comp[slot], 0));
@@ -256,7 +272,7 @@ int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t 
         VB_CUDA(cudaMemcpyAsync(st->h_tp[slot], st->d_tp[slot], (size_t)nb * hw * sizeof(float),
                                 cudaMemcpyDeviceToHost, st->s_d2h));
         if (corrected_host)
-            VB_CUDA(cudaMemcpyAsync(st->h_corr[slot], st->d_corr[slot], (size_t)nf * hw * sizeof(float),
+            VB_CUDA(cudaMemcpyAsync(st->h_corr[slot], corr, (size_t)nf * hw * sizeof(float),
                                     cudaMemcpyDeviceToHost, st->s_d2h));
         VB_CUDA(cudaEventRecord(st->ev_d2h[slot], st->s_d2h));
         if (k >= 1) rc = drain(k - 1);

@@ -45,7 +45,7 @@ __device__ __forceinline__ WarpOp make_warp(const vb_motion* vec, int64_t t) {
     op.ix = op.iy = 0;
     op.fx = op.fy = 0.f;
     op.omx = op.omy = 1.f;
-    if (!vec) return op;
+    if (!vec) return op;  // identity: the bilinear formula with zero weights returns the sample
     const vb_motion v = vec[t];
     const double vx = (double)v.dx + v.sub_dx, vy = (double)v.dy + v.sub_dy;  // MotionVector.x/.y
     if (vx == 0.0 && vy == 0.0) return op;                                     // motion.py:237-238
@@ -107,7 +107,6 @@ int launch_correct(const void* frames, int dtype, int64_t n, int h, int w, const
 // ------------------------------------------------------------------ K3
 constexpr int kTY = 32, kTX = 64, kK3Threads = 256;
 constexpr int kMaxWR = 16;
-constexpr int kPix = kTY * kTX / kK3Threads;  // pixels owned per thread
 
 struct Weights {
     double w[2 * kMaxWR + 1];  // centre at index wr (scipy weights reversed == same, symmetric)
@@ -116,84 +115,136 @@ struct Weights {
 struct K3Args {
     const void* frames;
     int dtype;
-    const vb_motion* vec;  // may be null: frames are already corrected
-    int64_t n;             // frames in this launch (from the first block start)
-    int h, w, L, wr;
+    const vb_motion* vec;  // may be null: frames are taken as they are (already corrected)
+    int64_t n;             // frames in this launch
+    int h, w, wr;
     Weights wt;
-    float* corrected;  // may be null
-    float* spatial;    // [blocks][h][w]
-    float* smoothed;   // [n][h][w] (time-major, block frames contiguous)
+    float* corrected;  // [n][h][w] or null
+    float* smoothed;   // [n][h][w]
 };
 
 // scipy correlate1d symmetric kernel: o = x0*w0; for j=-r..-1: o += (x[j]+x[-j])*w[j]
-__device__ __forceinline__ double corr_sym(const float* line, int stride, const double* wc, int r) {
-    double o = __dmul_rn((double)line[0], wc[0]);
+// (float64, unfused multiply/add as in the compiled C loop).
+__device__ __forceinline__ double corr_sym(const double* line, int stride, const double* wc, int r) {
+    double o = __dmul_rn(line[0], wc[0]);
     for (int j = -r; j < 0; ++j) {
-        const double pr = __dadd_rn((double)line[j * stride], (double)line[-j * stride]);
+        const double pr = __dadd_rn(line[j * stride], line[-j * stride]);
         o = __dadd_rn(o, __dmul_rn(pr, wc[j]));
     }
     return o;
 }
 
+static size_t k3_smem_bytes(int wr) {
+    const int EH = kTY + 2 * wr, EW = kTX + 2 * wr, EWP = EW | 1;
+    const size_t c = (size_t)EH * EWP * sizeof(double);
+    const size_t v = std::max((size_t)kTY * EWP * sizeof(double), (size_t)(EH + 1) * (EW + 1) * sizeof(float));
+    return c + v;
+}
+
+// One CTA per (frame, 32x64 tile).  Per frame: reflect/clamp index tables for
+// the tile + halo, the raw source box staged in shared memory, the corrected
+// samples (float32 bilinear in numpy's operation order; identity and integer
+// shifts are the same formula with zero weights), then the two separable
+// float64 passes.  The raw box aliases the vertical-pass buffer.
 __global__ void __launch_bounds__(kK3Threads) warp_smooth_kernel(K3Args a) {
-    extern __shared__ __align__(16) float sm3[];
+    extern __shared__ __align__(16) double sm3[];
     const int wr = a.wr;
-    const int EH = kTY + 2 * wr, EW = kTX + 2 * wr;
-    const int EWP = EW | 1;
-    float* sC = sm3;             // [EH][EWP]   corrected tile + halo
-    float* sV = sm3 + EH * EWP;  // [kTY][EWP]  after the H (vertical) pass
+    const int EH = kTY + 2 * wr, EW = kTX + 2 * wr, EWP = EW | 1;
+    double* sC = sm3;                                  // [EH][EWP] corrected tile + halo
+    double* sV = sm3 + (size_t)EH * EWP;               // [kTY][EWP] after the H pass
+    float* sRaw = reinterpret_cast<float*>(sV);        // raw source box (before sV is written)
     __shared__ double s_w[2 * kMaxWR + 1];
+    __shared__ int s_ra[kTY + 2 * kMaxWR], s_rc[kTY + 2 * kMaxWR];
+    __shared__ int s_xa[kTX + 2 * kMaxWR], s_xb[kTX + 2 * kMaxWR];
+    __shared__ int s_box[4];
     const int tid = threadIdx.x;
     if (tid < 2 * wr + 1) s_w[tid] = a.wt.w[tid];
-
-    const int ty0 = blockIdx.y * kTY, tx0 = blockIdx.x * kTX;
-    const int blk = blockIdx.z;
-    const int64_t t0 = (int64_t)blk * a.L;
-    const int64_t t1 = (t0 + a.L < a.n ? t0 + a.L : a.n);
-    const int64_t hw = (int64_t)a.h * a.w;
-    const int lx = tid % kTX, ly0 = tid / kTX;  // owned pixels: (ly0 + 4k, lx)
-    double sum[kPix];
-#pragma unroll
-    for (int k = 0; k < kPix; ++k) sum[k] = 0.0;
-    __syncthreads();
     const double* wc = s_w + wr;
+    const int ty0 = blockIdx.y * kTY, tx0 = blockIdx.x * kTX;
+    const int64_t hw = (int64_t)a.h * a.w;
 
-    for (int64_t t = t0; t < t1; ++t) {
+    for (int64_t t = blockIdx.z; t < a.n; t += gridDim.z) {
         const WarpOp op = make_warp(a.vec, t);
-        // 1. corrected frame on the tile + reflect halo
-        for (int i = tid; i < EH * EW; i += kK3Threads) {
-            const int ey = i / EW, ex = i - ey * EW;
-            const int gy = reflect_index(ty0 - wr + ey, a.h), gx = reflect_index(tx0 - wr + ex, a.w);
-            sC[ey * EWP + ex] = warp_sample(a.frames, a.dtype, t * hw, a.h, a.w, op, gy, gx);
+        if (tid < 4) s_box[tid] = (tid & 1) ? -1 : 0x7fffffff;
+        __syncthreads();
+        // 1. index tables: ext row ey -> source rows (ya, yc) of translate's a/c taps
+        for (int i = tid; i < EH + EW; i += kK3Threads) {
+            if (i < EH) {
+                const int y = reflect_index(ty0 - wr + i, a.h);
+                const int ya = clampi(y - op.iy, 0, a.h - 1), yc = clampi(y - op.iy - 1, 0, a.h - 1);
+                s_ra[i] = ya;
+                s_rc[i] = yc;
+                atomicMin(&s_box[0], min(ya, yc));
+                atomicMax(&s_box[1], max(ya, yc));
+            } else {
+                const int e = i - EH;
+                const int x = reflect_index(tx0 - wr + e, a.w);
+                const int xa = clampi(x - op.ix, 0, a.w - 1), xb = clampi(x - op.ix - 1, 0, a.w - 1);
+                s_xa[e] = xa;
+                s_xb[e] = xb;
+                atomicMin(&s_box[2], min(xa, xb));
+                atomicMax(&s_box[3], max(xa, xb));
+            }
         }
         __syncthreads();
-        // 2. own pixels: spatial sum + corrected output; then the H pass
-#pragma unroll
-        for (int k = 0; k < kPix; ++k) {
-            const int ly = ly0 + 4 * k, gy = ty0 + ly, gx = tx0 + lx;
-            const float c = sC[(ly + wr) * EWP + lx + wr];
-            sum[k] += (double)c;
-            if (a.corrected && gy < a.h && gx < a.w) a.corrected[t * hw + (int64_t)gy * a.w + gx] = c;
+        const int by0 = s_box[0], bx0 = s_box[2];
+        const int bh = s_box[1] - by0 + 1, bw = s_box[3] - bx0 + 1;
+        // 2. stage the raw source box (<= (EH+1) x (EW+1) samples)
+        const int64_t fb = t * hw;
+        for (int i = tid; i < bh * bw; i += kK3Threads) {
+            const int r = i / bw, c = i - r * bw;
+            sRaw[i] = load_sample(a.frames, a.dtype, fb + (int64_t)(by0 + r) * a.w + bx0 + c);
+        }
+        __syncthreads();
+        // 3. corrected samples on tile + halo
+        for (int i = tid; i < EH * EW; i += kK3Threads) {
+            const int ey = i / EW, ex = i - ey * EW;
+            const float* ra = sRaw + (s_ra[ey] - by0) * bw - bx0;
+            const float* rc = sRaw + (s_rc[ey] - by0) * bw - bx0;
+            const int xa = s_xa[ex], xb = s_xb[ex];
+            const float top = __fadd_rn(__fmul_rn(op.omx, ra[xa]), __fmul_rn(op.fx, ra[xb]));
+            const float bot = __fadd_rn(__fmul_rn(op.omx, rc[xa]), __fmul_rn(op.fx, rc[xb]));
+            sC[ey * EWP + ex] = (double)__fadd_rn(__fmul_rn(op.omy, top), __fmul_rn(op.fy, bot));
+        }
+        __syncthreads();
+        // 4. corrected output (interior) and the H (vertical) pass, rounded to f32
+        if (a.corrected) {
+            for (int i = tid; i < kTY * kTX; i += kK3Threads) {
+                const int ly = i / kTX, lx = i - ly * kTX;
+                const int gy = ty0 + ly, gx = tx0 + lx;
+                if (gy < a.h && gx < a.w) a.corrected[fb + (int64_t)gy * a.w + gx] = (float)sC[(ly + wr) * EWP + lx + wr];
+            }
         }
         for (int i = tid; i < kTY * EW; i += kK3Threads) {
             const int r = i / EW, c = i - r * EW;
-            sV[r * EWP + c] = (float)corr_sym(sC + (r + wr) * EWP + c, EWP, wc, wr);
+            sV[r * EWP + c] = (double)(float)corr_sym(sC + (r + wr) * EWP + c, EWP, wc, wr);
         }
         __syncthreads();
-        // 3. W pass on own pixels -> smoothed (time-major)
-#pragma unroll
-        for (int k = 0; k < kPix; ++k) {
-            const int ly = ly0 + 4 * k, gy = ty0 + ly, gx = tx0 + lx;
+        // 5. W pass -> smoothed frame (time-major)
+        for (int i = tid; i < kTY * kTX; i += kK3Threads) {
+            const int ly = i / kTX, lx = i - ly * kTX;
+            const int gy = ty0 + ly, gx = tx0 + lx;
             const float sv = (float)corr_sym(sV + ly * EWP + lx + wr, 1, wc, wr);
-            if (gy < a.h && gx < a.w) a.smoothed[t * hw + (int64_t)gy * a.w + gx] = sv;
+            if (gy < a.h && gx < a.w) a.smoothed[fb + (int64_t)gy * a.w + gx] = sv;
         }
+        __syncthreads();
     }
-    if (!a.spatial) return;
-    const double nblk = (double)(t1 - t0);
-#pragma unroll
-    for (int k = 0; k < kPix; ++k) {
-        const int gy = ty0 + ly0 + 4 * k, gx = tx0 + lx;
-        if (gy < a.h && gx < a.w) a.spatial[(int64_t)blk * hw + (int64_t)gy * a.w + gx] = (float)(sum[k] / nblk);
+}
+
+// Spatial summary (summarize.py:55-57): per-pixel float64 mean over the
+// block's corrected frames, accumulated sequentially in frame order like
+// numpy's axis-0 reduction -> bit-identical.
+__global__ void block_mean_kernel(const float* __restrict__ frames, int64_t n, int64_t hw, int L,
+                                  float* __restrict__ spatial) {
+    const int blk = blockIdx.y;
+    const int64_t t0 = (int64_t)blk * L;
+    const int cnt = (int)((int64_t)L < n - t0 ? (int64_t)L : n - t0);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hw; i += (int64_t)gridDim.x * blockDim.x) {
+        const float* col = frames + t0 * hw + i;
+        double s = 0.0;
+#pragma unroll 8
+        for (int t = 0; t < cnt; ++t) s += (double)__ldcs(col + (int64_t)t * hw);
+        spatial[(int64_t)blk * hw + i] = (float)(s / (double)cnt);
     }
 }
 
@@ -328,7 +379,10 @@ static int launch_median_vpl(const float* sm, int64_t n, int64_t hw, int L, int 
     const size_t smem = (size_t)L * (kK4Pix + 1) * sizeof(float);
     VB_CUDA(cudaFuncSetAttribute(median_kernel<VPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 grid((unsigned)((hw + kK4Pix - 1) / kK4Pix), (unsigned)nblk);
-    median_kernel<VPL><<<grid, kK4Threads, smem, s>>>(sm, n, hw, L, temporal);
+    {
+        ProfScope ps(kProfMedian, s);
+        median_kernel<VPL><<<grid, kK4Threads, smem, s>>>(sm, n, hw, L, temporal);
+    }
     VB_LAUNCHED();
     return VB_OK;
 }
@@ -342,8 +396,40 @@ static int launch_median(const float* sm, int64_t n, int64_t hw, int L, int nblk
     if (vpl <= 16) return launch_median_vpl<16>(sm, n, hw, L, nblk, temporal, s);
     if (vpl <= 32) return launch_median_vpl<32>(sm, n, hw, L, nblk, temporal, s);
     dim3 grid((unsigned)((hw + 3) / 4), (unsigned)nblk);
-    median_kernel_long<<<grid, 128, 0, s>>>(sm, n, hw, L, temporal);
+    {
+        ProfScope ps(kProfMedian, s);
+        median_kernel_long<<<grid, 128, 0, s>>>(sm, n, hw, L, temporal);
+    }
     VB_LAUNCHED();
+    return VB_OK;
+}
+
+static int launch_k3(const void* frames, int dtype, const vb_motion* vec, int64_t n, int h, int w,
+                     const double* weights, int wradius, float* corrected, float* smoothed, cudaStream_t s) {
+    K3Args a;
+    a.dtype = dtype;
+    a.h = h;
+    a.w = w;
+    a.wr = wradius;
+    for (int i = 0; i < 2 * wradius + 1; ++i) a.wt.w[i] = weights[i];
+    const size_t smem3 = k3_smem_bytes(wradius);
+    VB_CUDA(cudaFuncSetAttribute(warp_smooth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+    const int64_t hw = (int64_t)h * w;
+    const size_t esz = dtype == VB_U16 ? 2 : 4;
+    for (int64_t f0 = 0; f0 < n; f0 += 65535) {
+        const int64_t nf = std::min<int64_t>(65535, n - f0);
+        a.frames = (const char*)frames + (size_t)f0 * hw * esz;
+        a.vec = vec ? vec + f0 : nullptr;
+        a.n = nf;
+        a.corrected = corrected ? corrected + (size_t)f0 * hw : nullptr;
+        a.smoothed = smoothed + (size_t)f0 * hw;
+        dim3 grid((unsigned)((w + kTX - 1) / kTX), (unsigned)((h + kTY - 1) / kTY), (unsigned)nf);
+        {
+            ProfScope ps(kProfWarpSmooth, s);
+            warp_smooth_kernel<<<grid, kK3Threads, smem3, s>>>(a);
+        }
+        VB_LAUNCHED();
+    }
     return VB_OK;
 }
 
@@ -354,76 +440,56 @@ int launch_summarize(const void* frames, int dtype, const vb_motion* vec, int64_
     if (wradius > kMaxWR) return fail(VB_EINVAL, "smoothing radius too large (max 16)");
     const int64_t hw = (int64_t)h * w;
     const int64_t nblk_total = (n + seg_len - 1) / seg_len;
-    // blocks per launch: bound the smoothed scratch to ~4 GB
-    const size_t blk_bytes = (size_t)seg_len * hw * sizeof(float);
+    // blocks per batch: bound the smoothed (+ corrected) scratch to ~4 GB
+    const size_t blk_bytes = (size_t)seg_len * hw * sizeof(float) * (corrected ? 1 : 2);
     int64_t per = std::max<int64_t>(1, (int64_t)((size_t)4 << 30) / (int64_t)blk_bytes);
     per = std::min(per, nblk_total);
+    const size_t frame_bytes = (size_t)seg_len * per * hw * sizeof(float);
     float* smoothed = nullptr;
-    VB_CUDA(cudaMallocAsync(&smoothed, blk_bytes * per, s));
-    K3Args a;
-    a.dtype = dtype;
-    a.h = h;
-    a.w = w;
-    a.L = seg_len;
-    a.wr = wradius;
-    for (int i = 0; i < 2 * wradius + 1; ++i) a.wt.w[i] = weights[i];
-    const int EH = kTY + 2 * wradius, EWP = (kTX + 2 * wradius) | 1;
-    const size_t smem3 = (size_t)(EH + kTY) * EWP * sizeof(float);
-    cudaError_t e = cudaFuncSetAttribute(warp_smooth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
-    int rc = e == cudaSuccess ? VB_OK : cuda_fail(e, "cudaFuncSetAttribute(warp_smooth_kernel)");
+    float* corr_scratch = nullptr;
+    keep_pool();
+    VB_CUDA(cudaMallocAsync(&smoothed, frame_bytes, s));
+    if (!corrected) {
+        cudaError_t e = cudaMallocAsync(&corr_scratch, frame_bytes, s);
+        if (e != cudaSuccess) {
+            cudaFreeAsync(smoothed, s);
+            return cuda_fail(e, "cudaMallocAsync(corrected scratch)");
+        }
+    }
     const size_t esz = dtype == VB_U16 ? 2 : 4;
+    int rc = VB_OK;
     for (int64_t b0 = 0; b0 < nblk_total && rc == VB_OK; b0 += per) {
         const int nb = (int)std::min(per, nblk_total - b0);
         const int64_t f0 = b0 * seg_len;
         const int64_t nf = std::min<int64_t>((int64_t)nb * seg_len, n - f0);
-        a.frames = (const char*)frames + (size_t)f0 * hw * esz;
-        a.vec = vec ? vec + f0 : nullptr;
-        a.n = nf;
-        a.corrected = corrected ? corrected + (size_t)f0 * hw : nullptr;
-        a.spatial = spatial + (size_t)b0 * hw;
-        a.smoothed = smoothed;
-        dim3 grid((unsigned)((w + kTX - 1) / kTX), (unsigned)((h + kTY - 1) / kTY), (unsigned)nb);
-        warp_smooth_kernel<<<grid, kK3Threads, smem3, s>>>(a);
+        float* corr = corrected ? corrected + (size_t)f0 * hw : corr_scratch;
+        rc = launch_k3((const char*)frames + (size_t)f0 * hw * esz, dtype, vec ? vec + f0 : nullptr, nf, h, w, weights,
+                       wradius, corr, smoothed, s);
+        if (rc) break;
+        {
+            dim3 grid((unsigned)std::min<int64_t>((hw + 255) / 256, 1024), (unsigned)nb);
+            ProfScope ps(kProfOther, s);
+            block_mean_kernel<<<grid, 256, 0, s>>>(corr, nf, hw, seg_len, spatial + (size_t)b0 * hw);
+        }
         launches().fetch_add(1, std::memory_order_relaxed);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) { rc = cuda_fail(e, "warp_smooth_kernel"); break; }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) {
+            rc = cuda_fail(e, "block_mean_kernel");
+            break;
+        }
         rc = launch_median(smoothed, nf, hw, seg_len, nb, temporal + (size_t)b0 * hw, s);
     }
     cudaFreeAsync(smoothed, s);
+    if (corr_scratch) cudaFreeAsync(corr_scratch, s);
     return rc;
 }
 
-// Smoothing only (scipy gaussian_filter on each frame, summarize.py:60-73):
-// K3 with one-frame blocks, no warp and no spatial summary.
+// Smoothing only (scipy gaussian_filter on each frame, summarize.py:60-73).
 int launch_smooth(const void* frames, int dtype, int64_t n, int h, int w, const double* weights, int wradius,
                   float* out, cudaStream_t s) {
     if (n <= 0) return VB_OK;
     if (wradius > kMaxWR) return fail(VB_EINVAL, "smoothing radius too large (max 16)");
-    const int64_t hw = (int64_t)h * w;
-    K3Args a;
-    a.dtype = dtype;
-    a.vec = nullptr;
-    a.h = h;
-    a.w = w;
-    a.L = 1;
-    a.wr = wradius;
-    for (int i = 0; i < 2 * wradius + 1; ++i) a.wt.w[i] = weights[i];
-    a.corrected = nullptr;
-    a.spatial = nullptr;
-    const int EH = kTY + 2 * wradius, EWP = (kTX + 2 * wradius) | 1;
-    const size_t smem3 = (size_t)(EH + kTY) * EWP * sizeof(float);
-    VB_CUDA(cudaFuncSetAttribute(warp_smooth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
-    const size_t esz = dtype == VB_U16 ? 2 : 4;
-    for (int64_t f0 = 0; f0 < n; f0 += 65535) {
-        const int64_t nf = std::min<int64_t>(65535, n - f0);
-        a.frames = (const char*)frames + (size_t)f0 * hw * esz;
-        a.n = nf;
-        a.smoothed = out + (size_t)f0 * hw;
-        dim3 grid((unsigned)((w + kTX - 1) / kTX), (unsigned)((h + kTY - 1) / kTY), (unsigned)nf);
-        warp_smooth_kernel<<<grid, kK3Threads, smem3, s>>>(a);
-        VB_LAUNCHED();
-    }
-    return VB_OK;
+    return launch_k3(frames, dtype, nullptr, n, h, w, weights, wradius, nullptr, out, s);
 }
 
 }  // namespace vb

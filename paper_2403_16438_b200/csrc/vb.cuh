@@ -16,6 +16,7 @@ void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* where);
 std::atomic<int64_t>& launches();
+void keep_pool();
 
 #define VB_CUDA(call)                                               \
     do {                                                            \
@@ -29,6 +30,20 @@ std::atomic<int64_t>& launches();
         cudaError_t e_ = cudaGetLastError();                               \
         if (e_ != cudaSuccess) return ::vb::cuda_fail(e_, "kernel launch"); \
     } while (0)
+
+// ---- per-kernel CUDA-event profiler (vb_prof_enable / vb_prof_collect) ----
+enum KernelId { kProfZncc = 0, kProfFinalize = 1, kProfWarpSmooth = 2, kProfMedian = 3, kProfOther = 4,
+                kProfCount = 5 };
+class ProfScope {
+   public:
+    ProfScope(int id, cudaStream_t s);
+    ~ProfScope();
+
+   private:
+    int id_;
+    cudaStream_t s_;
+    cudaEvent_t a_ = nullptr, b_ = nullptr;
+};
 
 // ---- geometry ---------------------------------------------------------------
 // A patch group is a run of patches with the same origin y whose union window
@@ -60,6 +75,7 @@ struct Templates {
 int launch_template_sum(const void* frames, int dtype, int64_t n, int64_t hw, double* sum,
                         int accumulate, cudaStream_t s);
 int launch_template_finish(const double* sum, int64_t n_total, int64_t hw, float* ref, cudaStream_t s);
+size_t zncc_smem_bytes(int patch, int radius, int max_g, int max_wu);
 int launch_prep_templates(const float* ref, int h, int w, int patch, const Templates& t, cudaStream_t s);
 int launch_motion(const Templates& t, int h, int w, int patch, int radius, const void* frames, int dtype,
                   int64_t n_frames, int subpixel, vb_motion* vectors, double* scores, cudaStream_t s);

@@ -149,14 +149,17 @@ class HostStage:
         self.run_into(ptr, dtype, t, vec, sp, tp, corr)
         return vec, sp, tp, corr
 
-    def run_into(self, frames_ptr: int, dtype: int, t: int, vec, sp, tp, corr=None) -> None:
-        """Zero-allocation variant: all outputs are caller-provided host buffers
-        (numpy arrays or pinned torch tensors)."""
+    def run_into(self, frames_ptr: int, dtype: int, t: int, vec, sp, tp, corr=None,
+                 corrected_dev: torch.Tensor | None = None) -> None:
+        """Zero-allocation variant: outputs are caller-provided host buffers
+        (numpy arrays or pinned torch tensors); corrected_dev optionally keeps
+        the whole corrected video in HBM."""
         def p(x):
             if x is None:
                 return None
             return x.data_ptr() if isinstance(x, torch.Tensor) else x.ctypes.data
-        _lib.call("vb_stage_run_host", self._h, frames_ptr, dtype, t, p(vec), p(sp), p(tp), p(corr))
+        _lib.call("vb_stage_run_host", self._h, frames_ptr, dtype, t, p(vec), p(sp), p(tp), p(corr),
+                  D.ptr(corrected_dev))
 
     @property
     def last_launches(self) -> int:
