@@ -27,6 +27,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "vb.cuh"
@@ -110,10 +111,10 @@ struct ZnccArgs {
     int64_t hw;
     int w;
     int P, R, S, tp;
-    int dyc;  // dy rows per statistics chunk
     int nch;  // dx chunks per (patch, dy) item (1 on the fast path)
     int pitch_cap;
-    int off_inv, off_reg, off_scr;  // shared-memory carve-up (bytes)
+    int off_z;  // shared-memory carve-up (bytes): region at 0, cov buffer at off_z
+    int n_patches;
     const float* tmpl;
     const double* rvar;
     const double* rmean;
@@ -121,12 +122,131 @@ struct ZnccArgs {
     const PatchGroup* groups;
     int n_groups;
     int64_t n_frames;
+    float* inv;       // [n_frames][N][S*S]  1/sqrt(fvar*rvar) (0 where the reference skips)
     double* partial;  // [n_frames][n_groups][S*S]
 };
 
 constexpr int kGenericDXB = 8;
+constexpr int kStatsDC = 4;  // dy rows per vertical sliding chain in the statistics kernel
+
+// Frame samples are staged centred on an integer c close to the group's
+// template level, so the f32 cross sums accumulate O(100) instead of O(1000)
+// products.  Integer samples stay exact, and the window variance is shift
+// invariant, so the float64 statistics use the centred samples directly.
+// (Small-valued float data, |mean| < 64, is left uncentred.)
+__device__ __forceinline__ float group_centre(const ZnccArgs& a, const PatchGroup& grp) {
+    double m = 0.0;
+    for (int p = 0; p < grp.count; ++p) m += a.rmean[grp.first + p];
+    m /= (double)grp.count;
+    return fabs(m) >= 64.0 ? (float)rint(m) : 0.0f;
+}
+
+__device__ __forceinline__ void stage_region(const ZnccArgs& a, const PatchGroup& grp, int RH, int pitch, float cg,
+                                             int64_t t, float* s_reg) {
+    const int64_t fbase = t * a.hw;
+    const int wu = grp.wu;
+    for (int i = threadIdx.x; i < RH * wu; i += blockDim.x) {
+        const int r = i / wu, c = i - r * wu;
+        s_reg[r * pitch + c] =
+            __fsub_rn(load_sample(a.frames, a.dtype, fbase + (int64_t)(grp.y0 + r) * a.w + grp.x0 + c), cg);
+    }
+}
+
+// Window statistics for one (patch group, frame): sliding sums of f and f^2
+// over every candidate window, then inv = 1/sqrt(fvar * rvar) (kernels.py:60-72;
+// 0 where the reference skips a dead patch or a flat window).  Camera (u16)
+// samples use exact integer arithmetic (int32 sums, int64 sums of squares,
+// n*fvar = n*S2 - S1^2 exactly) -- no float conversions on the hot loop;
+// float32 input uses float64 sums.  Vertical chains run per (column, 4-row
+// chunk) so every thread has work; results go to global memory for the
+// search kernel.
+template <bool INT>
+__global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a) {
+    using T1 = typename std::conditional<INT, int, double>::type;        // sample / sum of f
+    using T2 = typename std::conditional<INT, long long, double>::type;  // sum of f^2
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int P = a.P, S = a.S, SS = S * S, R = (S - 1) / 2, RH = P + 2 * R;
+    const PatchGroup grp = a.groups[blockIdx.x];
+    const int G = grp.count, wu = grp.wu, pitch = a.pitch_cap, vp = wu | 1;
+    const double nn = (double)P * (double)P;
+    T1* s_reg = reinterpret_cast<T1*>(smem);                                   // [RH][pitch]
+    T2* v2 = reinterpret_cast<T2*>(smem + a.off_z);                            // [S][vp]
+    T1* v1 = reinterpret_cast<T1*>(smem + a.off_z + (size_t)S * a.pitch_cap * sizeof(T2));  // [S][vp]
+    const float cg = group_centre(a, grp);
+    const int cgi = (int)cg;
+    const int nchunk = (S + kStatsDC - 1) / kStatsDC;
+    for (int64_t t = blockIdx.y; t < a.n_frames; t += gridDim.y) {
+        __syncthreads();
+        {
+            const int64_t fbase = t * a.hw;
+            for (int i = threadIdx.x; i < RH * wu; i += blockDim.x) {
+                const int r = i / wu, c = i - r * wu;
+                const int64_t idx = fbase + (int64_t)(grp.y0 + r) * a.w + grp.x0 + c;
+                if constexpr (INT)
+                    s_reg[r * pitch + c] = (int)__ldg(reinterpret_cast<const uint16_t*>(a.frames) + idx) - cgi;
+                else
+                    s_reg[r * pitch + c] = (double)__fsub_rn(__ldg(reinterpret_cast<const float*>(a.frames) + idx), cg);
+            }
+        }
+        __syncthreads();
+        for (int it = threadIdx.x; it < wu * nchunk; it += blockDim.x) {
+            const int c = it % wu, k = it / wu;
+            const int d0 = k * kStatsDC, nd = min(kStatsDC, S - d0);
+            T1 s1 = 0;
+            T2 s2 = 0;
+            for (int yy = 0; yy < P; ++yy) {
+                const T1 f = s_reg[(d0 + yy) * pitch + c];
+                s1 += f;
+                s2 += (T2)f * (T2)f;
+            }
+            v1[d0 * vp + c] = s1;
+            v2[d0 * vp + c] = s2;
+            for (int j = 1; j < nd; ++j) {
+                const T1 fo = s_reg[(d0 + j - 1) * pitch + c];
+                const T1 fi = s_reg[(d0 + j - 1 + P) * pitch + c];
+                s1 += fi - fo;
+                s2 += (T2)fi * (T2)fi - (T2)fo * (T2)fo;
+                v1[(d0 + j) * vp + c] = s1;
+                v2[(d0 + j) * vp + c] = s2;
+            }
+        }
+        __syncthreads();
+        for (int it = threadIdx.x; it < G * S; it += blockDim.x) {
+            const int p = it / S, dy = it - p * S;
+            const int gp = grp.first + p;
+            const int col = a.patch_col[gp];
+            const double rv = a.rvar[gp];
+            const T1* r1 = v1 + dy * vp + col;
+            const T2* r2 = v2 + dy * vp + col;
+            T1 h1 = 0;
+            T2 h2 = 0;
+            for (int xx = 0; xx < P; ++xx) {
+                h1 += r1[xx];
+                h2 += r2[xx];
+            }
+            float* out = a.inv + ((size_t)t * a.n_patches + gp) * SS + (size_t)dy * S;
+            for (int dx = 0; dx < S; ++dx) {
+                float iv = 0.0f;
+                if constexpr (INT) {
+                    const long long nf = (long long)P * P * h2 - (long long)h1 * h1;  // n * fvar, exact
+                    if (rv > 0.0 && nf > 0) iv = (float)rsqrt((double)nf * rv / nn);
+                } else {
+                    const double fvar = h2 - h1 * h1 / nn;  // kernels.py:67
+                    if (rv > 0.0 && fvar > 0.0) iv = (float)rsqrt(fvar * rv);
+                }
+                out[dx] = iv;
+                if (dx + 1 < S) {
+                    h1 += r1[dx + P] - r1[dx];
+                    h2 += r2[dx + P] - r2[dx];
+                }
+            }
+        }
+    }
+}
 
 // Cross sums for one (patch, dy) row of S candidates, compile-time P and S.
+// Template taps come from the prepared patch in global memory (L1-resident,
+// warp-broadcast): every lane of a patch reads the same float4.
 template <int P, int S>
 __device__ __forceinline__ void cross_row(const float* __restrict__ reg, int pitch, const float* __restrict__ trow0,
                                           int tp, float (&acc)[S]) {
@@ -141,7 +261,7 @@ __device__ __forceinline__ void cross_row(const float* __restrict__ reg, int pit
         const float4* trow = reinterpret_cast<const float4*>(trow0 + yy * tp);
 #pragma unroll
         for (int q = 0; q < (P + 3) / 4; ++q) {
-            const float4 t4 = trow[q];
+            const float4 t4 = __ldg(trow + q);
             const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -155,7 +275,7 @@ __device__ __forceinline__ void cross_row(const float* __restrict__ reg, int pit
 }
 
 template <int P_CT, int S_CT>
-__global__ void __launch_bounds__(512, 1) zncc_group_kernel(ZnccArgs a) {
+__global__ void __launch_bounds__(256) zncc_group_kernel(ZnccArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int P = P_CT ? P_CT : a.P;
     const int S = S_CT ? S_CT : a.S;
@@ -164,99 +284,17 @@ __global__ void __launch_bounds__(512, 1) zncc_group_kernel(ZnccArgs a) {
     const int tp = a.tp;
     const PatchGroup grp = a.groups[blockIdx.x];
     const int G = grp.count;
-    const int wu = grp.wu;
     const int pitch = a.pitch_cap;  // odd, >= max wu
     const int SS = S * S;
-    const double nn = (double)P * (double)P;
-
-    // shared-memory carve-up (zncc_smem)
-    float* s_tmpl = reinterpret_cast<float*>(smem);                   // [G][P][tp]
-    float* s_inv = reinterpret_cast<float*>(smem + a.off_inv);        // [G][S*S]
-    float* s_reg = reinterpret_cast<float*>(smem + a.off_reg);        // [RH][pitch]
-    double* s_scr = reinterpret_cast<double*>(smem + a.off_scr);      // stats / z scratch
+    float* s_reg = reinterpret_cast<float*>(smem);             // [RH][pitch]
+    float* s_cov = reinterpret_cast<float*>(smem + a.off_z);   // [G][S*S]
     const int tid = threadIdx.x, nth = blockDim.x;
-
-    // templates + per-patch constants are frame independent
-    {
-        const float4* src = reinterpret_cast<const float4*>(a.tmpl + (size_t)grp.first * P * tp);
-        float4* dst = reinterpret_cast<float4*>(s_tmpl);
-        const int nv = G * P * tp / 4;
-        for (int i = tid; i < nv; i += nth) dst[i] = src[i];
-    }
-    // Frame samples are staged centred on an integer c close to the group's
-    // template level, so the f32 cross sums accumulate O(100) instead of
-    // O(1000) products.  Integer samples stay exact, and the window variance
-    // is shift invariant, so the float64 statistics use the centred samples
-    // directly.  (Small-valued float data, |mean| < 64, is left uncentred.)
-    float cg;
-    {
-        double m = 0.0;
-        for (int p = 0; p < G; ++p) m += a.rmean[grp.first + p];
-        m /= (double)G;
-        cg = fabs(m) >= 64.0 ? (float)rint(m) : 0.0f;
-    }
+    const float cg = group_centre(a, grp);
 
     for (int64_t t = blockIdx.y; t < a.n_frames; t += gridDim.y) {
         __syncthreads();  // previous frame fully consumed
-        // ---- stage the union window (raw samples, f32) ----
-        const int64_t fbase = t * a.hw;
-        for (int i = tid; i < RH * wu; i += nth) {
-            const int r = i / wu, c = i - r * wu;
-            s_reg[r * pitch + c] =
-                __fsub_rn(load_sample(a.frames, a.dtype, fbase + (int64_t)(grp.y0 + r) * a.w + grp.x0 + c), cg);
-        }
+        stage_region(a, grp, RH, pitch, cg, t, s_reg);
         __syncthreads();
-
-        // ---- window statistics: float64 sliding sums, DYC rows of dy at a time ----
-        for (int d0 = 0; d0 < S; d0 += a.dyc) {
-            const int nd = min(a.dyc, S - d0);
-            double* v1 = s_scr;                 // [dyc][wu]
-            double* v2 = s_scr + a.dyc * wu;    // [dyc][wu]
-            for (int c = tid; c < wu; c += nth) {
-                double s1 = 0.0, s2 = 0.0;
-                for (int yy = 0; yy < P; ++yy) {
-                    const double f = (double)s_reg[(d0 + yy) * pitch + c];
-                    s1 += f;
-                    s2 += f * f;
-                }
-                v1[c] = s1;
-                v2[c] = s2;
-                for (int k = 1; k < nd; ++k) {
-                    const double fo = (double)s_reg[(d0 + k - 1) * pitch + c];
-                    const double fi = (double)s_reg[(d0 + k - 1 + P) * pitch + c];
-                    s1 += fi - fo;
-                    s2 += fi * fi - fo * fo;
-                    v1[k * wu + c] = s1;
-                    v2[k * wu + c] = s2;
-                }
-            }
-            __syncthreads();
-            for (int it = tid; it < G * nd; it += nth) {
-                const int p = it / nd, k = it - p * nd;
-                const int col = a.patch_col[grp.first + p];
-                const double rv = a.rvar[grp.first + p];
-                const double* r1 = v1 + k * wu + col;
-                const double* r2 = v2 + k * wu + col;
-                double h1 = 0.0, h2 = 0.0;
-                for (int xx = 0; xx < P; ++xx) {
-                    h1 += r1[xx];
-                    h2 += r2[xx];
-                }
-                float* out = s_inv + (size_t)p * SS + (size_t)(d0 + k) * S;
-                for (int dx = 0; dx < S; ++dx) {
-                    const double fvar = h2 - h1 * h1 / nn;  // kernels.py:67
-                    out[dx] = (rv > 0.0 && fvar > 0.0) ? (float)(1.0 / sqrt(fvar * rv)) : 0.0f;
-                    if (dx + 1 < S) {
-                        h1 += r1[dx + P] - r1[dx];
-                        h2 += r2[dx + P] - r2[dx];
-                    }
-                }
-            }
-            __syncthreads();
-        }
-
-        // ---- cross term + normalisation ----
-        float* zbuf = reinterpret_cast<float*>(s_scr);  // [G][S*S]
         const int nitems = G * S * a.nch;
         for (int it = tid; it < nitems; it += nth) {
             const int dy = it % S;
@@ -264,14 +302,13 @@ __global__ void __launch_bounds__(512, 1) zncc_group_kernel(ZnccArgs a) {
             const int p = pc / a.nch, ch = pc - p * a.nch;
             const int col = a.patch_col[grp.first + p];
             const float* reg = s_reg + dy * pitch + col;
-            const float* trow0 = s_tmpl + (size_t)p * P * tp;
-            const float* inv = s_inv + (size_t)p * SS + dy * S;
-            float* z = zbuf + (size_t)p * SS + dy * S;
+            const float* trow0 = a.tmpl + (size_t)(grp.first + p) * P * tp;
+            float* z = s_cov + (size_t)p * SS + dy * S;
             if constexpr (P_CT != 0 && S_CT != 0) {
                 float acc[S_CT];
                 cross_row<P_CT, S_CT>(reg, pitch, trow0, tp, acc);
 #pragma unroll
-                for (int d = 0; d < S_CT; ++d) z[d] = acc[d] * inv[d];
+                for (int d = 0; d < S_CT; ++d) z[d] = acc[d];
             } else {
                 float acc[kGenericDXB];
 #pragma unroll
@@ -281,21 +318,24 @@ __global__ void __launch_bounds__(512, 1) zncc_group_kernel(ZnccArgs a) {
                     const float* fr = reg + yy * pitch + dx0;
                     const float* trow = trow0 + yy * tp;
                     for (int xx = 0; xx < P; ++xx) {
-                        const float tv = trow[xx];
+                        const float tv = __ldg(trow + xx);
 #pragma unroll
                         for (int d = 0; d < kGenericDXB; ++d) acc[d] = fmaf(fr[xx + d], tv, acc[d]);
                     }
                 }
 #pragma unroll
                 for (int d = 0; d < kGenericDXB; ++d)
-                    if (dx0 + d < S) z[dx0 + d] = acc[d] * inv[dx0 + d];
+                    if (dx0 + d < S) z[dx0 + d] = acc[d];
             }
         }
         __syncthreads();
+        // z = cov * inv (inv from the statistics kernel), summed over the
+        // group's patches in fixed order
         double* part = a.partial + ((size_t)t * a.n_groups + blockIdx.x) * SS;
+        const float* inv = a.inv + ((size_t)t * a.n_patches + grp.first) * SS;
         for (int c = tid; c < SS; c += nth) {
             double s = 0.0;
-            for (int p = 0; p < G; ++p) s += (double)zbuf[(size_t)p * SS + c];
+            for (int p = 0; p < G; ++p) s += (double)s_cov[(size_t)p * SS + c] * (double)__ldg(inv + (size_t)p * SS + c);
             part[c] = s;
         }
     }
@@ -409,32 +449,27 @@ static KernelFn pick_kernel(int P, int S, bool* fast) {
 }
 
 struct SmemPlan {
-    size_t off_inv, off_reg, off_scr, total;
-    int pitch, dyc;
+    size_t off_z, total;      // search kernel: region + cov buffer
+    size_t stats_total;       // statistics kernel: region + 2 x [S][wu] float64
+    int pitch;
 };
 
-static SmemPlan zncc_smem(int P, int R, int tp, int max_g, int max_wu) {
+static SmemPlan zncc_smem(int P, int R, int max_g, int max_wu) {
     const int S = 2 * R + 1, SS = S * S, RH = P + 2 * R;
     SmemPlan sp;
     sp.pitch = max_wu | 1;
-    sp.dyc = std::min(S, 4);
-    size_t off = 0;
-    off += (size_t)max_g * P * tp * 4;  // templates
-    sp.off_inv = off;
-    off += (size_t)max_g * SS * 4;      // inv
+    size_t off = (size_t)RH * sp.pitch * 4;
     off = (off + 15) & ~(size_t)15;
-    sp.off_reg = off;
-    off += (size_t)RH * sp.pitch * 4;
-    off = (off + 15) & ~(size_t)15;
-    sp.off_scr = off;
-    size_t scr = std::max((size_t)2 * sp.dyc * max_wu * 8, (size_t)max_g * SS * 4);
-    off += scr;
-    sp.total = off;
+    sp.off_z = off;
+    sp.total = off + (size_t)max_g * SS * 4;
+    // statistics kernel: region [RH][pitch] of int32/float64 + [S][pitch] sums
+    sp.stats_total = (((size_t)RH * sp.pitch * 8 + 15) & ~(size_t)15) + (size_t)S * sp.pitch * (8 + 8);
     return sp;
 }
 
 size_t zncc_smem_bytes(int patch, int radius, int max_g, int max_wu) {
-    return zncc_smem(patch, radius, (patch + 3) & ~3, max_g, max_wu).total;
+    SmemPlan sp = zncc_smem(patch, radius, max_g, max_wu);
+    return std::max(sp.total, sp.stats_total);
 }
 
 int launch_motion(const Templates& t, int h, int w, int patch, int radius, const void* frames, int dtype,
@@ -444,15 +479,17 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     const int S = 2 * radius + 1, SS = S * S;
     bool fast = false;
     KernelFn fn = pick_kernel(patch, S, &fast);
-    SmemPlan sp = zncc_smem(patch, radius, t.tp, t.max_g, t.max_wu);
-    if (sp.total > 227 * 1024) return fail(VB_EINVAL, "patch group does not fit in shared memory");
+    SmemPlan sp = zncc_smem(patch, radius, t.max_g, t.max_wu);
+    if (std::max(sp.total, sp.stats_total) > 227 * 1024)
+        return fail(VB_EINVAL, "patch group does not fit in shared memory");
     VB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.total));
+    void (*stats_fn)(ZnccArgs) = dtype == VB_U16 ? zncc_stats_kernel<true> : zncc_stats_kernel<false>;
+    const size_t reg_bytes = dtype == VB_U16 ? 4 : 8;
+    const size_t stats_off = (((size_t)(patch + 2 * radius) * sp.pitch * reg_bytes) + 15) & ~(size_t)15;
+    const size_t stats_smem = stats_off + (size_t)S * sp.pitch * (dtype == VB_U16 ? 8 + 4 : 8 + 8);
+    VB_CUDA(cudaFuncSetAttribute(stats_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stats_smem));
 
     ZnccArgs a;
-    a.off_inv = (int)sp.off_inv;
-    a.off_reg = (int)sp.off_reg;
-    a.off_scr = (int)sp.off_scr;
-    a.frames = frames;
     a.dtype = dtype;
     a.hw = (int64_t)h * w;
     a.w = w;
@@ -460,9 +497,10 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     a.R = radius;
     a.S = S;
     a.tp = t.tp;
-    a.dyc = sp.dyc;
     a.nch = fast ? 1 : (S + kGenericDXB - 1) / kGenericDXB;
     a.pitch_cap = sp.pitch;
+    a.off_z = (int)sp.off_z;
+    a.n_patches = t.n;
     a.tmpl = t.tmpl;
     a.rvar = t.rvar;
     a.rmean = t.rmean;
@@ -472,28 +510,45 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
 
     const int items = t.max_g * S * a.nch;
     int threads = ((items + 31) / 32) * 32;
-    threads = std::max(64, std::min(threads, 512));
+    threads = std::max(64, std::min(threads, 256));
 
-    // frame batches bound the float64 partial buffer to ~256 MB
-    const size_t per_frame = (size_t)t.n_groups * SS * sizeof(double);
-    int64_t batch = std::max<int64_t>(1, (int64_t)((256u << 20) / per_frame));
+    // frame batches bound the float64 partials + f32 inv buffers to ~1 GB
+    const size_t per_frame_part = (size_t)t.n_groups * SS * sizeof(double);
+    const size_t per_frame_inv = (size_t)t.n * SS * sizeof(float);
+    int64_t batch = std::max<int64_t>(1, (int64_t)(((size_t)1 << 30) / (per_frame_part + per_frame_inv)));
     batch = std::min(batch, n_frames);
     double* partial = nullptr;
+    float* inv = nullptr;
     keep_pool();
-    VB_CUDA(cudaMallocAsync(&partial, per_frame * batch, s));
+    VB_CUDA(cudaMallocAsync(&partial, per_frame_part * batch, s));
+    cudaError_t e0 = cudaMallocAsync(&inv, per_frame_inv * batch, s);
+    if (e0 != cudaSuccess) {
+        cudaFreeAsync(partial, s);
+        return cuda_fail(e0, "cudaMallocAsync(inv)");
+    }
     int rc = VB_OK;
     for (int64_t f0 = 0; f0 < n_frames && rc == VB_OK; f0 += batch) {
         const int64_t nb = std::min(batch, n_frames - f0);
         a.frames = (const char*)frames + (size_t)f0 * a.hw * (dtype == VB_U16 ? 2 : 4);
         a.n_frames = nb;
         a.partial = partial;
+        a.inv = inv;
         dim3 grid(t.n_groups, (unsigned)std::min<int64_t>(nb, 65535));
+        {
+            ProfScope ps(kProfOther, s);
+            ZnccArgs as = a;
+            as.off_z = (int)stats_off;
+            stats_fn<<<grid, 256, stats_smem, s>>>(as);
+        }
+        launches().fetch_add(1, std::memory_order_relaxed);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) { rc = cuda_fail(e, "zncc_stats_kernel"); break; }
         {
             ProfScope ps(kProfZncc, s);
             fn<<<grid, threads, sp.total, s>>>(a);
         }
         launches().fetch_add(1, std::memory_order_relaxed);
-        cudaError_t e = cudaGetLastError();
+        e = cudaGetLastError();
         if (e != cudaSuccess) { rc = cuda_fail(e, "zncc_group_kernel"); break; }
         const int fin_blocks = (int)std::min<int64_t>(nb, 148 * 8);
         {
@@ -506,6 +561,7 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
         if (e != cudaSuccess) { rc = cuda_fail(e, "finalize_kernel"); break; }
     }
     cudaFreeAsync(partial, s);
+    cudaFreeAsync(inv, s);
     return rc;
 }
 

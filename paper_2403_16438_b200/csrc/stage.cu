@@ -251,7 +251,7 @@ int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t 
     for (int64_t k = 0; k < nchunks && rc == VB_OK; ++k) {
         const int slot = (int)(k & 1);
         const int64_t f0 = k * C, nf = std::min<int64_t>(C, n_frames - f0);
-        const int64_t b0 = f0 / L, nb = (nf + L - 1) / L;
+        const int64_t nb = (nf + L - 1) / L;
         rc = upload(slot, f0, nf);
         if (rc) break;
         VB_CUDA(cudaStreamWaitEvent(st->s_comp, st->ev_h2d[slot], 0));
