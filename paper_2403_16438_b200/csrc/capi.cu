@@ -10,9 +10,40 @@
 #include <string>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
+#include "tma.cuh"
 #include "vb.cuh"
 
 namespace vb {
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point.
+bool make_frames_tmap(CUtensorMap* map, const void* base, int dtype, int64_t t, int h, int w, int bh, int bw) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        cudaGetLastError();
+    }
+    if (!encode || !base) return false;
+    const size_t esz = dtype == VB_U16 ? 2 : 4;
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || ((size_t)w * esz) % 16 || ((size_t)h * w * esz) % 16) return false;
+    if (bw < 1 || bh < 1 || bw > 256 || bh > 256 || ((size_t)bw * esz) % 16) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)(t > 0 ? t : 1)};
+    cuuint64_t strides[2] = {(cuuint64_t)(w * esz), (cuuint64_t)((size_t)h * w * esz)};
+    cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode(map, dtype == VB_U16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                        const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
 
 static thread_local std::string g_err;
 static std::atomic<int64_t> g_launches{0};

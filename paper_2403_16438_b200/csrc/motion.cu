@@ -25,11 +25,14 @@
 //    divides by N and runs the tie-broken argmax + quadratic fit: fully
 //    deterministic, no atomics.
 #include <math.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 #include <type_traits>
 #include <vector>
 
+#include "tma.cuh"
 #include "vb.cuh"
 
 namespace vb {
@@ -106,14 +109,18 @@ int launch_prep_templates(const float* ref, int h, int w, int patch, const Templ
 
 // ---------------------------------------------------------------- ZNCC
 struct ZnccArgs {
-    const void* frames;
+    const void* frames;  // first frame of this launch
     int dtype;
     int64_t hw;
     int w;
     int P, R, S, tp;
-    int nch;  // dx chunks per (patch, dy) item (1 on the fast path)
-    int pitch_cap;
-    int off_z;  // shared-memory carve-up (bytes): region at 0, cov buffer at off_z
+    int nch;        // dx chunks per (patch, dy) item (1 on the fast path)
+    int pitch_cap;  // f32 region pitch (odd, >= max wu)
+    int bw, bh;     // raw box width / height in samples (bh = P + 2R)
+    int bhc;        // TMA box height (the raw box is fetched as ceil(bh/bhc) row chunks)
+    int use_tma;
+    int tma_z0;     // tensor-map frame index of this launch's frame 0
+    int off_reg, off_z;  // shared-memory carve-up (bytes); raw box at 0
     int n_patches;
     const float* tmpl;
     const double* rvar;
@@ -129,11 +136,10 @@ struct ZnccArgs {
 constexpr int kGenericDXB = 8;
 constexpr int kStatsDC = 4;  // dy rows per vertical sliding chain in the statistics kernel
 
-// Frame samples are staged centred on an integer c close to the group's
-// template level, so the f32 cross sums accumulate O(100) instead of O(1000)
-// products.  Integer samples stay exact, and the window variance is shift
-// invariant, so the float64 statistics use the centred samples directly.
-// (Small-valued float data, |mean| < 64, is left uncentred.)
+// Frame samples are centred on an integer c close to the group's template
+// level, so the f32 cross sums accumulate O(100) instead of O(1000)
+// products.  Integer samples stay exact; the window variance is shift
+// invariant.  (Small-valued float data, |mean| < 64, is left uncentred.)
 __device__ __forceinline__ float group_centre(const ZnccArgs& a, const PatchGroup& grp) {
     double m = 0.0;
     for (int p = 0; p < grp.count; ++p) m += a.rmean[grp.first + p];
@@ -141,14 +147,46 @@ __device__ __forceinline__ float group_centre(const ZnccArgs& a, const PatchGrou
     return fabs(m) >= 64.0 ? (float)rint(m) : 0.0f;
 }
 
-__device__ __forceinline__ void stage_region(const ZnccArgs& a, const PatchGroup& grp, int RH, int pitch, float cg,
-                                             int64_t t, float* s_reg) {
+// Column offset of the group window inside its raw box: TMA tile loads on
+// sm_100a fault (illegal instruction) unless the innermost start coordinate
+// is 16-byte aligned, so boxes start at the aligned column below x0.
+__device__ __forceinline__ int box_off(const ZnccArgs& a, const PatchGroup& grp) {
+    return grp.x0 & (a.dtype == VB_U16 ? 7 : 3);
+}
+
+// Raw box [bh][bw] of frame t (group union window) -> shared memory.  With
+// TMA one elected thread issues cp.async.bulk.tensor row chunks completing on
+// `bar`; otherwise all threads copy (caller synchronises).
+__device__ __forceinline__ void fetch_box(const ZnccArgs& a, const CUtensorMap* tmap, const PatchGroup& grp,
+                                          int64_t t, void* raw, uint64_t* bar) {
+    const size_t esz = a.dtype == VB_U16 ? 2 : 4;
+    if (a.use_tma) {
+        if (threadIdx.x == 0) {
+            const int nck = (a.bh + a.bhc - 1) / a.bhc;
+            mbar_expect_tx(bar, (uint32_t)((size_t)a.bw * a.bhc * nck * esz));
+            for (int k = 0; k < nck; ++k)
+                tma_load_3d((char*)raw + (size_t)k * a.bhc * a.bw * esz, tmap, grp.x0 - box_off(a, grp),
+                            grp.y0 + k * a.bhc, a.tma_z0 + (int)t, bar);
+        }
+        return;
+    }
     const int64_t fbase = t * a.hw;
-    const int wu = grp.wu;
-    for (int i = threadIdx.x; i < RH * wu; i += blockDim.x) {
-        const int r = i / wu, c = i - r * wu;
-        s_reg[r * pitch + c] =
-            __fsub_rn(load_sample(a.frames, a.dtype, fbase + (int64_t)(grp.y0 + r) * a.w + grp.x0 + c), cg);
+    const int wu = grp.wu, off = box_off(a, grp);
+    for (int i = threadIdx.x; i < a.bh * wu; i += blockDim.x) {
+        const int r = i / wu, cc = i - r * wu;
+        const int64_t idx = fbase + (int64_t)(grp.y0 + r) * a.w + grp.x0 + cc;
+        if (a.dtype == VB_U16)
+            reinterpret_cast<uint16_t*>(raw)[r * a.bw + cc + off] =
+                __ldg(reinterpret_cast<const uint16_t*>(a.frames) + idx);
+        else
+            reinterpret_cast<float*>(raw)[r * a.bw + cc + off] = __ldg(reinterpret_cast<const float*>(a.frames) + idx);
+    }
+}
+
+__device__ __forceinline__ void box_ready(const ZnccArgs& a, uint64_t* bar, uint32_t& phase) {
+    if (a.use_tma) {
+        mbar_wait(bar, phase);
+        phase ^= 1u;
     }
 }
 
@@ -156,54 +194,59 @@ __device__ __forceinline__ void stage_region(const ZnccArgs& a, const PatchGroup
 // over every candidate window, then inv = 1/sqrt(fvar * rvar) (kernels.py:60-72;
 // 0 where the reference skips a dead patch or a flat window).  Camera (u16)
 // samples use exact integer arithmetic (int32 sums, int64 sums of squares,
-// n*fvar = n*S2 - S1^2 exactly) -- no float conversions on the hot loop;
-// float32 input uses float64 sums.  Vertical chains run per (column, 4-row
-// chunk) so every thread has work; results go to global memory for the
-// search kernel.
+// n*fvar = n*S2 - S1^2 exactly) straight from the TMA-staged raw box; float32
+// input uses float64 sums.  Vertical chains run per (column, 4-row chunk) so
+// every thread has work.  The next frame's box is fetched while this frame's
+// horizontal pass runs.
 template <bool INT>
-__global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a) {
+__global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __grid_constant__ CUtensorMap tmap) {
     using T1 = typename std::conditional<INT, int, double>::type;        // sample / sum of f
     using T2 = typename std::conditional<INT, long long, double>::type;  // sum of f^2
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int P = a.P, S = a.S, SS = S * S, R = (S - 1) / 2, RH = P + 2 * R;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar;
+    const int P = a.P, S = a.S, SS = S * S, R = (S - 1) / 2;
+    (void)R;
     const PatchGroup grp = a.groups[blockIdx.x];
-    const int G = grp.count, wu = grp.wu, pitch = a.pitch_cap, vp = wu | 1;
+    const int G = grp.count, wu = grp.wu, vp = wu | 1;
     const double nn = (double)P * (double)P;
-    T1* s_reg = reinterpret_cast<T1*>(smem);                                   // [RH][pitch]
-    T2* v2 = reinterpret_cast<T2*>(smem + a.off_z);                            // [S][vp]
+    T2* v2 = reinterpret_cast<T2*>(smem + a.off_z);                                         // [S][vp]
     T1* v1 = reinterpret_cast<T1*>(smem + a.off_z + (size_t)S * a.pitch_cap * sizeof(T2));  // [S][vp]
     const float cg = group_centre(a, grp);
     const int cgi = (int)cg;
     const int nchunk = (S + kStatsDC - 1) / kStatsDC;
-    for (int64_t t = blockIdx.y; t < a.n_frames; t += gridDim.y) {
-        __syncthreads();
-        {
-            const int64_t fbase = t * a.hw;
-            for (int i = threadIdx.x; i < RH * wu; i += blockDim.x) {
-                const int r = i / wu, c = i - r * wu;
-                const int64_t idx = fbase + (int64_t)(grp.y0 + r) * a.w + grp.x0 + c;
-                if constexpr (INT)
-                    s_reg[r * pitch + c] = (int)__ldg(reinterpret_cast<const uint16_t*>(a.frames) + idx) - cgi;
-                else
-                    s_reg[r * pitch + c] = (double)__fsub_rn(__ldg(reinterpret_cast<const float*>(a.frames) + idx), cg);
-            }
-        }
-        __syncthreads();
+    const int boff = box_off(a, grp);
+    if (threadIdx.x == 0 && a.use_tma) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+        tma_prefetch_desc(&tmap);
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    int64_t t = blockIdx.y;
+    if (t < a.n_frames) fetch_box(a, &tmap, grp, t, smem, &bar);
+    for (; t < a.n_frames; t += gridDim.y) {
+        __syncthreads();  // box visible (plain path) / V free (previous horizontal pass done)
+        box_ready(a, &bar, phase);
         for (int it = threadIdx.x; it < wu * nchunk; it += blockDim.x) {
             const int c = it % wu, k = it / wu;
             const int d0 = k * kStatsDC, nd = min(kStatsDC, S - d0);
+            auto sample = [&](int r) -> T1 {
+                if constexpr (INT)
+                    return (int)reinterpret_cast<const uint16_t*>(smem)[r * a.bw + c + boff] - cgi;
+                else
+                    return (double)__fsub_rn(reinterpret_cast<const float*>(smem)[r * a.bw + c + boff], cg);
+            };
             T1 s1 = 0;
             T2 s2 = 0;
             for (int yy = 0; yy < P; ++yy) {
-                const T1 f = s_reg[(d0 + yy) * pitch + c];
+                const T1 f = sample(d0 + yy);
                 s1 += f;
                 s2 += (T2)f * (T2)f;
             }
             v1[d0 * vp + c] = s1;
             v2[d0 * vp + c] = s2;
             for (int j = 1; j < nd; ++j) {
-                const T1 fo = s_reg[(d0 + j - 1) * pitch + c];
-                const T1 fi = s_reg[(d0 + j - 1 + P) * pitch + c];
+                const T1 fo = sample(d0 + j - 1), fi = sample(d0 + j - 1 + P);
                 s1 += fi - fo;
                 s2 += (T2)fi * (T2)fi - (T2)fo * (T2)fo;
                 v1[(d0 + j) * vp + c] = s1;
@@ -211,6 +254,7 @@ __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a) {
             }
         }
         __syncthreads();
+        if (t + gridDim.y < a.n_frames) fetch_box(a, &tmap, grp, t + gridDim.y, smem, &bar);  // raw box is free
         for (int it = threadIdx.x; it < G * S; it += blockDim.x) {
             const int p = it / S, dy = it - p * S;
             const int gp = grp.first + p;
@@ -274,27 +318,57 @@ __device__ __forceinline__ void cross_row(const float* __restrict__ reg, int pit
     }
 }
 
+// Search kernel: persistent over frames (blockIdx.y, +gridDim.y, ...).  Per
+// frame: wait for the TMA box, convert it to the centred f32 region, issue
+// the next frame's TMA into the now-free raw buffer, run the register-tiled
+// cross sums, then z = cov * inv summed over the group's patches in fixed
+// order.
 template <int P_CT, int S_CT>
-__global__ void __launch_bounds__(256) zncc_group_kernel(ZnccArgs a) {
-    extern __shared__ __align__(16) unsigned char smem[];
+__global__ void __launch_bounds__(256) zncc_group_kernel(ZnccArgs a, const __grid_constant__ CUtensorMap tmap) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar;
     const int P = P_CT ? P_CT : a.P;
     const int S = S_CT ? S_CT : a.S;
     const int R = (S - 1) / 2;
     const int RH = P + 2 * R;
     const int tp = a.tp;
     const PatchGroup grp = a.groups[blockIdx.x];
-    const int G = grp.count;
-    const int pitch = a.pitch_cap;  // odd, >= max wu
+    const int G = grp.count, wu = grp.wu;
+    const int pitch = a.pitch_cap;
     const int SS = S * S;
-    float* s_reg = reinterpret_cast<float*>(smem);             // [RH][pitch]
-    float* s_cov = reinterpret_cast<float*>(smem + a.off_z);   // [G][S*S]
+    float* s_reg = reinterpret_cast<float*>(smem + a.off_reg);  // [RH][pitch]
+    float* s_cov = reinterpret_cast<float*>(smem + a.off_z);    // [G][S*S]
     const int tid = threadIdx.x, nth = blockDim.x;
     const float cg = group_centre(a, grp);
-
-    for (int64_t t = blockIdx.y; t < a.n_frames; t += gridDim.y) {
-        __syncthreads();  // previous frame fully consumed
-        stage_region(a, grp, RH, pitch, cg, t, s_reg);
+    const float magic = 8388608.0f + cg;
+    const int boff = box_off(a, grp);
+    if (tid == 0 && a.use_tma) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+        tma_prefetch_desc(&tmap);
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    int64_t t = blockIdx.y;
+    if (t < a.n_frames) fetch_box(a, &tmap, grp, t, smem, &bar);
+    for (; t < a.n_frames; t += gridDim.y) {
+        __syncthreads();  // plain-path box visible; region/cov of the previous frame consumed
+        box_ready(a, &bar, phase);
+        if (a.dtype == VB_U16) {
+            const uint16_t* raw = reinterpret_cast<const uint16_t*>(smem);
+            for (int i = tid; i < RH * wu; i += nth) {
+                const int r = i / wu, c = i - r * wu;
+                s_reg[r * pitch + c] = u16_minus(raw[r * a.bw + c + boff], magic);
+            }
+        } else {
+            const float* raw = reinterpret_cast<const float*>(smem);
+            for (int i = tid; i < RH * wu; i += nth) {
+                const int r = i / wu, c = i - r * wu;
+                s_reg[r * pitch + c] = __fsub_rn(raw[r * a.bw + c + boff], cg);
+            }
+        }
         __syncthreads();
+        if (t + gridDim.y < a.n_frames) fetch_box(a, &tmap, grp, t + gridDim.y, smem, &bar);  // raw box is free
         const int nitems = G * S * a.nch;
         for (int it = tid; it < nitems; it += nth) {
             const int dy = it % S;
@@ -329,8 +403,6 @@ __global__ void __launch_bounds__(256) zncc_group_kernel(ZnccArgs a) {
             }
         }
         __syncthreads();
-        // z = cov * inv (inv from the statistics kernel), summed over the
-        // group's patches in fixed order
         double* part = a.partial + ((size_t)t * a.n_groups + blockIdx.x) * SS;
         const float* inv = a.inv + ((size_t)t * a.n_patches + grp.first) * SS;
         for (int c = tid; c < SS; c += nth) {
@@ -418,7 +490,7 @@ __global__ void finalize_kernel(const double* __restrict__ partial, int n_groups
 }
 
 // ---------------------------------------------------------------- launcher
-using KernelFn = void (*)(ZnccArgs);
+using KernelFn = void (*)(ZnccArgs, CUtensorMap);
 
 template <int S>
 static KernelFn fast_kernel_for() {
@@ -449,45 +521,50 @@ static KernelFn pick_kernel(int P, int S, bool* fast) {
 }
 
 struct SmemPlan {
-    size_t off_z, total;      // search kernel: region + cov buffer
-    size_t stats_total;       // statistics kernel: region + 2 x [S][wu] float64
-    int pitch;
+    int bw, bh, bhc, pitch;
+    size_t raw_bytes;          // raw box (TMA destination), offset 0
+    size_t off_reg, off_z;     // search kernel: f32 region, cov buffer
+    size_t total;              // search kernel
+    size_t stats_off, stats_total;  // statistics kernel: raw box + [S][pitch] T2 + [S][pitch] T1
 };
 
-static SmemPlan zncc_smem(int P, int R, int max_g, int max_wu) {
+static SmemPlan zncc_smem(int P, int R, int max_g, int max_wu, int dtype) {
     const int S = 2 * R + 1, SS = S * S, RH = P + 2 * R;
+    const size_t esz = dtype == VB_U16 ? 2 : 4;
     SmemPlan sp;
+    sp.bh = RH;
+    // TMA box rows are 16-byte multiples and start 16-byte aligned (up to
+    // 16/esz - 1 extra leading columns)
+    sp.bw = (int)((((max_wu + 16 / esz - 1) * esz + 15) / 16) * 16 / esz);
     sp.pitch = max_wu | 1;
-    size_t off = (size_t)RH * sp.pitch * 4;
-    off = (off + 15) & ~(size_t)15;
-    sp.off_z = off;
-    sp.total = off + (size_t)max_g * SS * 4;
-    // statistics kernel: region [RH][pitch] of int32/float64 + [S][pitch] sums
-    sp.stats_total = (((size_t)RH * sp.pitch * 8 + 15) & ~(size_t)15) + (size_t)S * sp.pitch * (8 + 8);
+    sp.bhc = std::min(sp.bh, 256);  // TMA box height limit (one chunk for P + 2R <= 256)
+    const int rows = (sp.bh + sp.bhc - 1) / sp.bhc * sp.bhc;
+    sp.raw_bytes = (((size_t)sp.bw * rows * esz) + 127) & ~(size_t)127;
+    sp.off_reg = sp.raw_bytes;
+    sp.off_z = (sp.off_reg + (size_t)RH * sp.pitch * 4 + 15) & ~(size_t)15;
+    sp.total = sp.off_z + (size_t)max_g * SS * 4;
+    sp.stats_off = sp.raw_bytes;
+    sp.stats_total = sp.stats_off + (size_t)S * sp.pitch * (dtype == VB_U16 ? 8 + 4 : 8 + 8);
     return sp;
 }
 
 size_t zncc_smem_bytes(int patch, int radius, int max_g, int max_wu) {
-    SmemPlan sp = zncc_smem(patch, radius, max_g, max_wu);
+    SmemPlan sp = zncc_smem(patch, radius, max_g, max_wu, VB_F32);  // f32 is the larger layout
     return std::max(sp.total, sp.stats_total);
 }
 
 int launch_motion(const Templates& t, int h, int w, int patch, int radius, const void* frames, int dtype,
                   int64_t n_frames, int subpixel, vb_motion* vectors, double* scores, cudaStream_t s) {
-    (void)h;
     if (n_frames <= 0) return VB_OK;
     const int S = 2 * radius + 1, SS = S * S;
     bool fast = false;
     KernelFn fn = pick_kernel(patch, S, &fast);
-    SmemPlan sp = zncc_smem(patch, radius, t.max_g, t.max_wu);
+    void (*stats_fn)(ZnccArgs, CUtensorMap) = dtype == VB_U16 ? zncc_stats_kernel<true> : zncc_stats_kernel<false>;
+    SmemPlan sp = zncc_smem(patch, radius, t.max_g, t.max_wu, dtype);
     if (std::max(sp.total, sp.stats_total) > 227 * 1024)
         return fail(VB_EINVAL, "patch group does not fit in shared memory");
     VB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.total));
-    void (*stats_fn)(ZnccArgs) = dtype == VB_U16 ? zncc_stats_kernel<true> : zncc_stats_kernel<false>;
-    const size_t reg_bytes = dtype == VB_U16 ? 4 : 8;
-    const size_t stats_off = (((size_t)(patch + 2 * radius) * sp.pitch * reg_bytes) + 15) & ~(size_t)15;
-    const size_t stats_smem = stats_off + (size_t)S * sp.pitch * (dtype == VB_U16 ? 8 + 4 : 8 + 8);
-    VB_CUDA(cudaFuncSetAttribute(stats_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stats_smem));
+    VB_CUDA(cudaFuncSetAttribute(stats_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.stats_total));
 
     ZnccArgs a;
     a.dtype = dtype;
@@ -499,7 +576,9 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     a.tp = t.tp;
     a.nch = fast ? 1 : (S + kGenericDXB - 1) / kGenericDXB;
     a.pitch_cap = sp.pitch;
-    a.off_z = (int)sp.off_z;
+    a.bw = sp.bw;
+    a.bh = sp.bh;
+    a.bhc = sp.bhc;
     a.n_patches = t.n;
     a.tmpl = t.tmpl;
     a.rvar = t.rvar;
@@ -507,6 +586,11 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     a.patch_col = t.patch_col;
     a.groups = t.groups;
     a.n_groups = t.n_groups;
+    // one tensor map over the whole launch range (frames as the z dimension)
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof(tmap));
+    static const bool no_tma = getenv("VB_NO_TMA") != nullptr;  // debug toggle: plain-load staging
+    a.use_tma = !no_tma && make_frames_tmap(&tmap, frames, dtype, n_frames, h, w, sp.bhc, sp.bw) ? 1 : 0;
 
     const int items = t.max_g * S * a.nch;
     int threads = ((items + 31) / 32) * 32;
@@ -526,26 +610,37 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
         cudaFreeAsync(partial, s);
         return cuda_fail(e0, "cudaMallocAsync(inv)");
     }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int rc = VB_OK;
     for (int64_t f0 = 0; f0 < n_frames && rc == VB_OK; f0 += batch) {
         const int64_t nb = std::min(batch, n_frames - f0);
         a.frames = (const char*)frames + (size_t)f0 * a.hw * (dtype == VB_U16 ? 2 : 4);
+        a.tma_z0 = (int)f0;
         a.n_frames = nb;
         a.partial = partial;
         a.inv = inv;
-        dim3 grid(t.n_groups, (unsigned)std::min<int64_t>(nb, 65535));
+        // persistent CTAs: each walks frames y, y+gy, ... (about 8 frames per CTA)
+        const int64_t want_y = std::max<int64_t>(1, (int64_t)sms * 8 * 4 / std::max(1, t.n_groups));
+        const unsigned gy = (unsigned)std::min<int64_t>(std::min<int64_t>(nb, 65535), std::max<int64_t>(want_y, (nb + 7) / 8));
+        dim3 grid(t.n_groups, gy);
         {
-            ProfScope ps(kProfOther, s);
             ZnccArgs as = a;
-            as.off_z = (int)stats_off;
-            stats_fn<<<grid, 256, stats_smem, s>>>(as);
+            as.off_reg = 0;
+            as.off_z = (int)sp.stats_off;
+            ProfScope ps(kProfOther, s);
+            stats_fn<<<grid, 256, sp.stats_total, s>>>(as, tmap);
         }
         launches().fetch_add(1, std::memory_order_relaxed);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) { rc = cuda_fail(e, "zncc_stats_kernel"); break; }
         {
+            ZnccArgs as = a;
+            as.off_reg = (int)sp.off_reg;
+            as.off_z = (int)sp.off_z;
             ProfScope ps(kProfZncc, s);
-            fn<<<grid, threads, sp.total, s>>>(a);
+            fn<<<grid, threads, sp.total, s>>>(as, tmap);
         }
         launches().fetch_add(1, std::memory_order_relaxed);
         e = cudaGetLastError();
