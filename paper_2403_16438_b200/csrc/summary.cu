@@ -28,6 +28,12 @@
 
 #include <algorithm>
 
+#include <stdlib.h>
+#include <string.h>
+
+#include <type_traits>
+
+#include "tma.cuh"
 #include "vb.cuh"
 
 namespace vb {
@@ -273,6 +279,175 @@ __global__ void __launch_bounds__(kK3Threads, 3) warp_smooth_kernel(K3Args a) {
     }
 }
 
+// Rows (or columns) of the source frame that the corrected tile + halo
+// touches: reflect(lo .. hi-1) shifted by -i0 and -(i0+1), clamped.  Exact
+// for a single reflection (n >= the halo); otherwise the whole axis.
+__device__ __forceinline__ void src_span(int lo, int hi, int n, int i0, int& a0, int& a1) {
+    int mn, mx;
+    if (-lo <= n && hi - n <= n) {
+        mn = lo < 0 ? 0 : (hi > n ? min(lo, 2 * n - hi) : lo);
+        mx = hi > n ? n - 1 : (lo < 0 ? max(hi - 1, -lo - 1) : hi - 1);
+    } else {
+        mn = 0;
+        mx = n - 1;
+    }
+    a0 = clampi(mn - i0 - 1, 0, n - 1);
+    a1 = clampi(mx - i0, 0, n - 1);
+}
+
+// K3 with compile-time tile geometry and a TMA-prefetched raw box: one CTA
+// per (tile, frame slice), persistent over frames z, z+gz, ...  The elected
+// thread issues the next frame's box (16-byte aligned start, zero-filled out
+// of bounds) as soon as the current box has been consumed, so the global
+// latency overlaps the two float64 passes.
+template <int WR, bool U16>
+__global__ void __launch_bounds__(kK3Threads, 3) warp_smooth_tma_kernel(K3Args a, const __grid_constant__ CUtensorMap tmap) {
+    constexpr int EH = kTY + 2 * WR, EW = kTX + 2 * WR, EWP = EW | 1;
+    constexpr int ALN = U16 ? 8 : 4;                                   // 16-byte alignment in samples
+    constexpr int BWB = ((EW + 1 + ALN - 1 + ALN - 1) / ALN) * ALN;    // box width
+    constexpr int BHB = EH + 1;                                        // box height
+    using S_T = typename std::conditional<U16, uint16_t, float>::type;
+    extern __shared__ __align__(128) unsigned char smem[];
+    S_T* sRaw = reinterpret_cast<S_T*>(smem);                                          // [BHB][BWB]
+    double* sC = reinterpret_cast<double*>(smem + (((size_t)BHB * BWB * sizeof(S_T) + 127) & ~(size_t)127));  // [EH][EWP]
+    double* sV = sC + (size_t)EH * EWP;                                                // [kTY][EWP]
+    __shared__ double s_w[WR + 1];
+    __shared__ int s_ra[EH], s_rc[EH], s_xa[EW], s_xb[EW];
+    __shared__ int s_box[2];
+    __shared__ __align__(8) uint64_t bar;
+    const int tid = threadIdx.x;
+    if (tid <= WR) s_w[tid] = a.wt.w[WR - tid];  // s_w[k] = weight at offset -k (symmetric)
+    const int ty0 = blockIdx.y * kTY, tx0 = blockIdx.x * kTX;
+    const int64_t hw = (int64_t)a.h * a.w;
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+        tma_prefetch_desc(&tmap);
+    }
+    __syncthreads();
+    // elected thread: issue frame t's box; returns its origin via s_box
+    auto issue = [&](int64_t t) {
+        const WarpOp op = make_warp(a.vec, t);
+        int y0, y1, x0, x1;
+        src_span(ty0 - WR, ty0 + kTY + WR, a.h, op.iy, y0, y1);
+        src_span(tx0 - WR, tx0 + kTX + WR, a.w, op.ix, x0, x1);
+        const int x0a = x0 & ~(ALN - 1);
+        mbar_expect_tx(&bar, (uint32_t)(BWB * BHB * sizeof(S_T)));
+        tma_load_3d(sRaw, &tmap, x0a, y0, (int)t, &bar);
+        return make_int2(x0a, y0);
+    };
+    int2 origin_next = make_int2(0, 0);
+    int64_t t = blockIdx.z;
+    if (tid == 0 && t < a.n) origin_next = issue(t);
+    uint32_t phase = 0;
+    const double* wk = s_w;  // wk[k] = w(-k)
+    for (; t < a.n; t += gridDim.z) {
+        const WarpOp op = make_warp(a.vec, t);
+        if (tid == 0) {
+            s_box[0] = origin_next.x;
+            s_box[1] = origin_next.y;
+        }
+        // 1. index tables (all threads; the box origin is published with them)
+        for (int i = tid; i < EH + EW; i += kK3Threads) {
+            if (i < EH) {
+                const int y = reflect_index(ty0 - WR + i, a.h);
+                s_ra[i] = clampi(y - op.iy, 0, a.h - 1);
+                s_rc[i] = clampi(y - op.iy - 1, 0, a.h - 1);
+            } else {
+                const int e = i - EH;
+                const int x = reflect_index(tx0 - WR + e, a.w);
+                s_xa[e] = clampi(x - op.ix, 0, a.w - 1);
+                s_xb[e] = clampi(x - op.ix - 1, 0, a.w - 1);
+            }
+        }
+        __syncthreads();
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+        const int bx0 = s_box[0], by0 = s_box[1];
+        // 2. corrected samples on tile + halo (float32, numpy's order); the
+        //    interior goes straight to the corrected output
+        for (int i = tid; i < EH * EW; i += kK3Threads) {
+            const int ey = i / EW, ex = i - ey * EW;
+            const S_T* ra = sRaw + (s_ra[ey] - by0) * BWB - bx0;
+            const S_T* rc = sRaw + (s_rc[ey] - by0) * BWB - bx0;
+            const int xa = s_xa[ex], xb = s_xb[ex];
+            const float top = __fadd_rn(__fmul_rn(op.omx, (float)ra[xa]), __fmul_rn(op.fx, (float)ra[xb]));
+            const float bot = __fadd_rn(__fmul_rn(op.omx, (float)rc[xa]), __fmul_rn(op.fx, (float)rc[xb]));
+            const float v = __fadd_rn(__fmul_rn(op.omy, top), __fmul_rn(op.fy, bot));
+            sC[ey * EWP + ex] = (double)v;
+            if (a.corrected && ey >= WR && ey < WR + kTY && ex >= WR && ex < WR + kTX) {
+                const int gy = ty0 + ey - WR, gx = tx0 + ex - WR;
+                if (gy < a.h && gx < a.w) a.corrected[t * hw + (int64_t)gy * a.w + gx] = v;
+            }
+        }
+        __syncthreads();
+        if (tid == 0 && t + gridDim.z < a.n) origin_next = issue(t + gridDim.z);  // raw box consumed
+        // 3. H (vertical) pass, VR outputs per thread, rounded to f32
+        constexpr int VR = 4, HR = 8;
+        for (int i = tid; i < (kTY / VR) * EW; i += kK3Threads) {
+            const int c = i % EW, r0 = (i / EW) * VR;
+            double x[VR + 2 * WR];
+#pragma unroll
+            for (int q = 0; q < VR + 2 * WR; ++q) x[q] = sC[(r0 + q) * EWP + c];
+#pragma unroll
+            for (int j = 0; j < VR; ++j) {
+                double acc = __dmul_rn(x[j + WR], wk[0]);
+#pragma unroll
+                for (int k = WR; k >= 1; --k) acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(x[j + WR - k], x[j + WR + k]), wk[k]));
+                sV[(r0 + j) * EWP + c] = (double)(float)acc;
+            }
+        }
+        __syncthreads();
+        // 4. W pass -> smoothed frame (time-major)
+        for (int i = tid; i < kTY * (kTX / HR); i += kK3Threads) {
+            const int ly = i / (kTX / HR), lx0 = (i % (kTX / HR)) * HR;
+            double x[HR + 2 * WR];
+#pragma unroll
+            for (int q = 0; q < HR + 2 * WR; ++q) x[q] = sV[ly * EWP + lx0 + q];
+            const int gy = ty0 + ly;
+#pragma unroll
+            for (int j = 0; j < HR; ++j) {
+                double acc = __dmul_rn(x[j + WR], wk[0]);
+#pragma unroll
+                for (int k = WR; k >= 1; --k) acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(x[j + WR - k], x[j + WR + k]), wk[k]));
+                const int gx = tx0 + lx0 + j;
+                if (gy < a.h && gx < a.w) a.smoothed[t * hw + (int64_t)gy * a.w + gx] = (float)acc;
+            }
+        }
+    }
+}
+
+template <int WR, bool U16>
+static size_t k3_tma_smem_bytes() {
+    constexpr int EH = kTY + 2 * WR, EW = kTX + 2 * WR, EWP = EW | 1;
+    constexpr int ALN = U16 ? 8 : 4;
+    constexpr int BWB = ((EW + 1 + ALN - 1 + ALN - 1) / ALN) * ALN;
+    constexpr int BHB = EH + 1;
+    const size_t raw = (((size_t)BHB * BWB * (U16 ? 2 : 4)) + 127) & ~(size_t)127;
+    return raw + (size_t)(EH + kTY) * EWP * sizeof(double);
+}
+
+template <int WR, bool U16>
+static int launch_k3_tma(const CUtensorMap& tmap, K3Args a, int64_t n, int h, int w, cudaStream_t s) {
+    const size_t smem = k3_tma_smem_bytes<WR, U16>();
+    auto kern = warp_smooth_tma_kernel<WR, U16>;
+    VB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int tiles = ((w + kTX - 1) / kTX) * ((h + kTY - 1) / kTY);
+    // ~4 frames per CTA, at least 8 resident waves of CTAs
+    const int64_t gz = std::min<int64_t>(65535, std::max<int64_t>((n + 3) / 4, ((int64_t)sms * 24 + tiles - 1) / tiles));
+    a.n = n;
+    dim3 grid((unsigned)((w + kTX - 1) / kTX), (unsigned)((h + kTY - 1) / kTY), (unsigned)std::min<int64_t>(gz, n));
+    {
+        ProfScope ps(kProfWarpSmooth, s);
+        kern<<<grid, kK3Threads, smem, s>>>(a, tmap);
+    }
+    VB_LAUNCHED();
+    return VB_OK;
+}
+
 // Spatial summary (summarize.py:55-57): per-pixel float64 mean over the
 // block's corrected frames, accumulated sequentially in frame order like
 // numpy's axis-0 reduction -> bit-identical.
@@ -454,6 +629,21 @@ static int launch_k3(const void* frames, int dtype, const vb_motion* vec, int64_
     a.w = w;
     a.wr = wradius;
     for (int i = 0; i < 2 * wradius + 1; ++i) a.wt.w[i] = weights[i];
+    static const bool no_tma = getenv("VB_NO_TMA") != nullptr;
+    if (wradius == 9 && !no_tma && n <= 0x7fffffff) {
+        constexpr int EH = kTY + 18, EW = kTX + 18;
+        CUtensorMap tmap;
+        memset(&tmap, 0, sizeof(tmap));
+        const int bwb = dtype == VB_U16 ? ((EW + 1 + 14) / 8) * 8 : ((EW + 1 + 6) / 4) * 4;
+        if (make_frames_tmap(&tmap, frames, dtype, n, h, w, EH + 1, bwb)) {
+            a.frames = frames;
+            a.vec = vec;
+            a.corrected = corrected;
+            a.smoothed = smoothed;
+            return dtype == VB_U16 ? launch_k3_tma<9, true>(tmap, a, n, h, w, s)
+                                   : launch_k3_tma<9, false>(tmap, a, n, h, w, s);
+        }
+    }
     const size_t smem3 = k3_smem_bytes(wradius);
     void (*kern)(K3Args) = wradius == 9 ? warp_smooth_kernel<9> : warp_smooth_kernel<0>;
     VB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
