@@ -371,8 +371,15 @@ __global__ void __launch_bounds__(kK3Threads, 3) warp_smooth_tma_kernel(K3Args a
             const S_T* ra = sRaw + (s_ra[ey] - by0) * BWB - bx0;
             const S_T* rc = sRaw + (s_rc[ey] - by0) * BWB - bx0;
             const int xa = s_xa[ex], xb = s_xb[ex];
-            const float top = __fadd_rn(__fmul_rn(op.omx, (float)ra[xa]), __fmul_rn(op.fx, (float)ra[xb]));
-            const float bot = __fadd_rn(__fmul_rn(op.omx, (float)rc[xa]), __fmul_rn(op.fx, (float)rc[xb]));
+            // u16 -> f32 exactly on the ALU/FMA pipes (no I2F on the conversion unit)
+            auto smp = [](S_T v) -> float {
+                if constexpr (U16)
+                    return u16_minus(v, 8388608.0f);
+                else
+                    return v;
+            };
+            const float top = __fadd_rn(__fmul_rn(op.omx, smp(ra[xa])), __fmul_rn(op.fx, smp(ra[xb])));
+            const float bot = __fadd_rn(__fmul_rn(op.omx, smp(rc[xa])), __fmul_rn(op.fx, smp(rc[xb])));
             const float v = __fadd_rn(__fmul_rn(op.omy, top), __fmul_rn(op.fy, bot));
             sC[ey * EWP + ex] = (double)v;
             if (a.corrected && ey >= WR && ey < WR + kTY && ex >= WR && ex < WR + kTX) {
@@ -398,20 +405,33 @@ __global__ void __launch_bounds__(kK3Threads, 3) warp_smooth_tma_kernel(K3Args a
             }
         }
         __syncthreads();
-        // 4. W pass -> smoothed frame (time-major)
+        // 4. W pass -> smoothed frame (time-major).  Lanes take consecutive
+        //    rows (bank-conflict-free float64 reads), each HR consecutive outputs.
         for (int i = tid; i < kTY * (kTX / HR); i += kK3Threads) {
-            const int ly = i / (kTX / HR), lx0 = (i % (kTX / HR)) * HR;
+            const int ly = i % kTY, lx0 = (i / kTY) * HR;
             double x[HR + 2 * WR];
 #pragma unroll
             for (int q = 0; q < HR + 2 * WR; ++q) x[q] = sV[ly * EWP + lx0 + q];
             const int gy = ty0 + ly;
+            float o[HR];
 #pragma unroll
             for (int j = 0; j < HR; ++j) {
                 double acc = __dmul_rn(x[j + WR], wk[0]);
 #pragma unroll
                 for (int k = WR; k >= 1; --k) acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(x[j + WR - k], x[j + WR + k]), wk[k]));
-                const int gx = tx0 + lx0 + j;
-                if (gy < a.h && gx < a.w) a.smoothed[t * hw + (int64_t)gy * a.w + gx] = (float)acc;
+                o[j] = (float)acc;
+            }
+            const int gx0 = tx0 + lx0;
+            float* dst = a.smoothed + t * hw + (int64_t)gy * a.w + gx0;
+            if (gy < a.h) {
+                if ((a.w & 3) == 0 && gx0 + HR <= a.w) {
+#pragma unroll
+                    for (int j = 0; j < HR; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < HR; ++j)
+                        if (gx0 + j < a.w) dst[j] = o[j];
+                }
             }
         }
     }
