@@ -354,17 +354,18 @@ __global__ void __launch_bounds__(256) zncc_group_kernel(ZnccArgs a, const __gri
     for (; t < a.n_frames; t += gridDim.y) {
         __syncthreads();  // plain-path box visible; region/cov of the previous frame consumed
         box_ready(a, &bar, phase);
-        if (a.dtype == VB_U16) {
-            const uint16_t* raw = reinterpret_cast<const uint16_t*>(smem);
-            for (int i = tid; i < RH * wu; i += nth) {
-                const int r = i / wu, c = i - r * wu;
-                s_reg[r * pitch + c] = u16_minus(raw[r * a.bw + c + boff], magic);
-            }
-        } else {
-            const float* raw = reinterpret_cast<const float*>(smem);
-            for (int i = tid; i < RH * wu; i += nth) {
-                const int r = i / wu, c = i - r * wu;
-                s_reg[r * pitch + c] = __fsub_rn(raw[r * a.bw + c + boff], cg);
+        // raw box -> centred f32 region: warps over rows, lanes over columns
+        // (no per-element index division)
+        {
+            const int lane = tid & 31, nw = nth >> 5;
+            if (a.dtype == VB_U16) {
+                const uint16_t* raw = reinterpret_cast<const uint16_t*>(smem) + boff;
+                for (int r = tid >> 5; r < RH; r += nw)
+                    for (int c = lane; c < wu; c += 32) s_reg[r * pitch + c] = u16_minus(raw[r * a.bw + c], magic);
+            } else {
+                const float* raw = reinterpret_cast<const float*>(smem) + boff;
+                for (int r = tid >> 5; r < RH; r += nw)
+                    for (int c = lane; c < wu; c += 32) s_reg[r * pitch + c] = __fsub_rn(raw[r * a.bw + c], cg);
             }
         }
         __syncthreads();
