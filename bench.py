@@ -310,13 +310,23 @@ def run_ours(args):
     _lib.check(L.vb_fp32_peak_probe(_lib.C.byref(p2), _lib.C.byref(p1)))
     fp32_peak = max(p2.value, p1.value)
     step_ms = elapsed / args.steps
+    traffic, traffic_src = None, None
+    tj = ROOT / "profiles" / "ncu_traffic.json"
+    if tj.exists():
+        try:
+            z = json.loads(tj.read_text())["zncc_group_kernel"]
+            traffic = z["dram_bytes_per_frame"] * frames_per_launch
+            traffic_src = z["source"] + "; scaled to this run's frames per launch"
+        except (ValueError, KeyError):
+            pass
     kernel_ms_per_step = {n: float(ms[i] / args.steps) for i, n in
                           enumerate(["zncc_group", "finalize", "warp_smooth", "median", "other"])}
     hbm_stage = bytes_frame * t / (step_ms / 1e3) / 1e9
     roofline = {
         "bound": "fp32", "kernel": "zncc_group_kernel<21,17>",
         "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
-        "traffic": None,
+        "traffic": traffic,
+        "traffic_source": traffic_src,
         "peak_source": "measured live: FFMA2 (fma.rn.f32x2) probe, vb_fp32_peak_probe",
         "peak_ffma_scalar": p1.value,
         "algorithmic": f"{flops_frame:.4g} flop/frame = 2*N_patch({n_patches})*(2r+1)^2*21^2; "
