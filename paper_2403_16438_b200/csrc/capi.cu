@@ -3,6 +3,7 @@
 // entry point replaces.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -116,34 +117,88 @@ static void free_templates(Templates& t) {
     t = Templates();
 }
 
-// Group consecutive patches that share an origin row into CTA work units.
+// Group consecutive patches that share an origin row into CTA work units:
+// each run of equal-y patches is split into ceil(run / max_g) groups of
+// near-equal size (balanced CTAs).
 static void build_groups(const std::vector<int32_t>& o, int patch, int radius, int max_g,
                          std::vector<PatchGroup>& groups, std::vector<int32_t>& col) {
     const int n = (int)o.size() / 2;
     col.assign(n, 0);
     int i = 0;
     while (i < n) {
-        PatchGroup g;
-        memset(&g, 0, sizeof(g));
-        g.first = i;
-        int j = i + 1;
-        int minx = o[2 * i], maxx = o[2 * i];
-        while (j < n && j - i < max_g && o[2 * j + 1] == o[2 * i + 1]) {
-            const int x = o[2 * j];
-            const int nmin = std::min(minx, x), nmax = std::max(maxx, x);
-            if (nmax - nmin > (max_g - 1) * patch + patch) break;  // keep the union compact
-            minx = nmin;
-            maxx = nmax;
-            ++j;
+        // run of patches on the same row whose union stays compact
+        int run = 1;
+        int rmin = o[2 * i], rmax = o[2 * i];
+        while (i + run < n && o[2 * (i + run) + 1] == o[2 * i + 1]) {
+            const int x = o[2 * (i + run)];
+            const int nmin = std::min(rmin, x), nmax = std::max(rmax, x);
+            if (nmax - nmin > (run + 1) * patch) break;
+            rmin = nmin;
+            rmax = nmax;
+            ++run;
         }
-        g.count = j - i;
-        g.x0 = minx - radius;
-        g.y0 = o[2 * i + 1] - radius;
-        g.wu = maxx - minx + patch + 2 * radius;
-        for (int k = i; k < j; ++k) col[k] = o[2 * k] - minx;
-        groups.push_back(g);
-        i = j;
+        const int k = (run + max_g - 1) / max_g;
+        for (int q = 0, start = i; q < k; ++q) {
+            const int cnt = run / k + (q < run % k ? 1 : 0);
+            PatchGroup g;
+            memset(&g, 0, sizeof(g));
+            g.first = start;
+            g.count = cnt;
+            int minx = o[2 * start], maxx = o[2 * start];
+            for (int j = start; j < start + cnt; ++j) {
+                minx = std::min(minx, (int)o[2 * j]);
+                maxx = std::max(maxx, (int)o[2 * j]);
+            }
+            g.x0 = minx - radius;
+            g.y0 = o[2 * start + 1] - radius;
+            g.wu = maxx - minx + patch + 2 * radius;
+            for (int j = start; j < start + cnt; ++j) col[j] = o[2 * j] - minx;
+            groups.push_back(g);
+            start += cnt;
+        }
+        i += run;
     }
+}
+
+// Pick the group size: lane efficiency of the (patch, dy[, dx-chunk]) item
+// loop times an occupancy factor, subject to the shared-memory budget.
+static int choose_group_size(const std::vector<int32_t>& o, int patch, int radius) {
+    const int S = 2 * radius + 1;
+    const int nch = (patch == 21 && S <= 25) ? 1 : (S + 7) / 8;
+    double best = -1.0;
+    int best_g = 1;
+    std::vector<PatchGroup> groups;
+    std::vector<int32_t> col;
+    for (int g = 1; g <= kMaxGroup; ++g) {
+        groups.clear();
+        build_groups(o, patch, radius, g, groups, col);
+        int mg = 0, mw = 0;
+        long long items = 0;
+        for (auto& x : groups) {
+            mg = std::max(mg, (int)x.count);
+            mw = std::max(mw, (int)x.wu);
+            items += (long long)x.count * S * nch;
+        }
+        // feasibility with the larger (f32-input) layout; occupancy for camera (u16) input
+        if (zncc_smem_bytes(patch, radius, mg, mw, VB_F32) > 160 * 1024 && g > 1) break;
+        const size_t smem = zncc_search_smem_bytes(patch, radius, mg, mw, VB_U16);
+        const int max_items = mg * S * nch;
+        const int threads = std::max(64, std::min(256, (max_items + 31) / 32 * 32));
+        const int rounds = (max_items + threads - 1) / threads;
+        const double lane_eff = (double)items / ((double)groups.size() * rounds * threads);
+        // measured (G sweep, C2): >= 4 resident CTAs per SM with L1 headroom for
+        // the broadcast template taps beats larger groups with fewer CTAs
+        const int by_smem = (int)((228 * 1024) / (smem + 1024));
+        const int by_regs = 65536 / (threads * 72);
+        const int ctas = std::max(1, std::min(std::min(by_smem, by_regs), 32));
+        const double occ = std::min(1.0, ctas / 4.0);
+        const double score = lane_eff * occ;
+        if (score > best + 1e-9) {
+            best = score;
+            best_g = g;
+        }
+    }
+    return best_g;
 }
 
 extern "C" {
@@ -192,18 +247,10 @@ int vb_motion_plan_create(vb_motion_plan** out, int height, int width, int patch
     std::vector<int32_t> col;
     // group width: ~8 patches keeps the CTA at <= ~80 KB of shared memory;
     // shrink the group until the search CTA fits (large radii)
-    int max_g = std::max(1, std::min(kMaxGroup, patch >= 16 ? 8 : 12));
-    for (;;) {
-        groups.clear();
-        build_groups(p->origins, patch, radius, max_g, groups, col);
-        int mg = 0, mw = 0;
-        for (auto& g : groups) {
-            mg = std::max(mg, (int)g.count);
-            mw = std::max(mw, (int)g.wu);
-        }
-        if (zncc_smem_bytes(patch, radius, mg, mw) <= 160 * 1024 || max_g == 1) break;
-        max_g = std::max(1, max_g / 2);
-    }
+    static const char* force_g = getenv("VB_GROUP");  // experiment knob: fixed patches per group
+    const int max_g = force_g ? std::max(1, std::min(kMaxGroup, atoi(force_g)))
+                              : choose_group_size(p->origins, patch, radius);
+    build_groups(p->origins, patch, radius, max_g, groups, col);
     Templates& t = p->t;
     t.n = n_origins;
     t.n_groups = (int)groups.size();

@@ -120,7 +120,7 @@ struct ZnccArgs {
     int bhc;        // TMA box height (the raw box is fetched as ceil(bh/bhc) row chunks)
     int use_tma;
     int tma_z0;     // tensor-map frame index of this launch's frame 0
-    int off_reg, off_z;  // shared-memory carve-up (bytes); raw box at 0
+    int off_reg, off_z, off_t;  // shared-memory carve-up (bytes); raw box at 0
     int n_patches;
     const float* tmpl;
     const double* rvar;
@@ -338,7 +338,14 @@ __global__ void __launch_bounds__(256) zncc_group_kernel(ZnccArgs a, const __gri
     const int SS = S * S;
     float* s_reg = reinterpret_cast<float*>(smem + a.off_reg);  // [RH][pitch]
     float* s_cov = reinterpret_cast<float*>(smem + a.off_z);    // [G][S*S]
+    float* s_tmpl = reinterpret_cast<float*>(smem + a.off_t);   // [G][P][tp] (fast path)
     const int tid = threadIdx.x, nth = blockDim.x;
+    constexpr bool kTmplSmem = false;  // measured: L1-resident taps beat an smem copy (occupancy)
+    if constexpr (kTmplSmem && P_CT != 0 && S_CT != 0) {
+        const float4* src = reinterpret_cast<const float4*>(a.tmpl + (size_t)grp.first * P * tp);
+        float4* dst = reinterpret_cast<float4*>(s_tmpl);
+        for (int i = tid; i < G * P * tp / 4; i += nth) dst[i] = __ldg(src + i);
+    }
     const float cg = group_centre(a, grp);
     const float magic = 8388608.0f + cg;
     const int boff = box_off(a, grp);
@@ -377,7 +384,8 @@ __global__ void __launch_bounds__(256) zncc_group_kernel(ZnccArgs a, const __gri
             const int p = pc / a.nch, ch = pc - p * a.nch;
             const int col = a.patch_col[grp.first + p];
             const float* reg = s_reg + dy * pitch + col;
-            const float* trow0 = a.tmpl + (size_t)(grp.first + p) * P * tp;
+            const float* trow0 = (kTmplSmem && P_CT != 0 && S_CT != 0) ? s_tmpl + (size_t)p * P * tp
+                                                                       : a.tmpl + (size_t)(grp.first + p) * P * tp;
             float* z = s_cov + (size_t)p * SS + dy * S;
             if constexpr (P_CT != 0 && S_CT != 0) {
                 float acc[S_CT];
@@ -525,6 +533,7 @@ struct SmemPlan {
     int bw, bh, bhc, pitch;
     size_t raw_bytes;          // raw box (TMA destination), offset 0
     size_t off_reg, off_z;     // search kernel: f32 region, cov buffer
+    size_t off_t;              // search kernel: template patches (fast path)
     size_t total;              // search kernel
     size_t stats_off, stats_total;  // statistics kernel: raw box + [S][pitch] T2 + [S][pitch] T1
 };
@@ -543,15 +552,20 @@ static SmemPlan zncc_smem(int P, int R, int max_g, int max_wu, int dtype) {
     sp.raw_bytes = (((size_t)sp.bw * rows * esz) + 127) & ~(size_t)127;
     sp.off_reg = sp.raw_bytes;
     sp.off_z = (sp.off_reg + (size_t)RH * sp.pitch * 4 + 15) & ~(size_t)15;
-    sp.total = sp.off_z + (size_t)max_g * SS * 4;
+    sp.off_t = (sp.off_z + (size_t)max_g * SS * 4 + 15) & ~(size_t)15;
+    sp.total = sp.off_t;  // + max_g * P * tp * 4 with kTmplSmem
     sp.stats_off = sp.raw_bytes;
     sp.stats_total = sp.stats_off + (size_t)S * sp.pitch * (dtype == VB_U16 ? 8 + 4 : 8 + 8);
     return sp;
 }
 
-size_t zncc_smem_bytes(int patch, int radius, int max_g, int max_wu) {
-    SmemPlan sp = zncc_smem(patch, radius, max_g, max_wu, VB_F32);  // f32 is the larger layout
+size_t zncc_smem_bytes(int patch, int radius, int max_g, int max_wu, int dtype) {
+    SmemPlan sp = zncc_smem(patch, radius, max_g, max_wu, dtype);
     return std::max(sp.total, sp.stats_total);
+}
+
+size_t zncc_search_smem_bytes(int patch, int radius, int max_g, int max_wu, int dtype) {
+    return zncc_smem(patch, radius, max_g, max_wu, dtype).total;
 }
 
 int launch_motion(const Templates& t, int h, int w, int patch, int radius, const void* frames, int dtype,
@@ -640,6 +654,7 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
             ZnccArgs as = a;
             as.off_reg = (int)sp.off_reg;
             as.off_z = (int)sp.off_z;
+            as.off_t = (int)sp.off_t;
             ProfScope ps(kProfZncc, s);
             fn<<<grid, threads, sp.total, s>>>(as, tmap);
         }

@@ -75,7 +75,8 @@ struct Templates {
 int launch_template_sum(const void* frames, int dtype, int64_t n, int64_t hw, double* sum,
                         int accumulate, cudaStream_t s);
 int launch_template_finish(const double* sum, int64_t n_total, int64_t hw, float* ref, cudaStream_t s);
-size_t zncc_smem_bytes(int patch, int radius, int max_g, int max_wu);
+size_t zncc_smem_bytes(int patch, int radius, int max_g, int max_wu, int dtype);  // search + stats kernels
+size_t zncc_search_smem_bytes(int patch, int radius, int max_g, int max_wu, int dtype);
 int launch_prep_templates(const float* ref, int h, int w, int patch, const Templates& t, cudaStream_t s);
 int launch_motion(const Templates& t, int h, int w, int patch, int radius, const void* frames, int dtype,
                   int64_t n_frames, int subpixel, vb_motion* vectors, double* scores, cudaStream_t s);
