@@ -134,7 +134,7 @@ struct ZnccArgs {
 };
 
 constexpr int kGenericDXB = 8;
-constexpr int kStatsDC = 4;  // dy rows per vertical sliding chain in the statistics kernel
+constexpr int kStatsDC = 6;  // dy rows per vertical sliding chain in the statistics kernel
 
 // Frame samples are centred on an integer c close to the group's template
 // level, so the f32 cross sums accumulate O(100) instead of O(1000)
@@ -272,8 +272,13 @@ __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __gri
             for (int dx = 0; dx < S; ++dx) {
                 float iv = 0.0f;
                 if constexpr (INT) {
-                    const long long nf = (long long)P * P * h2 - (long long)h1 * h1;  // n * fvar, exact
-                    if (rv > 0.0 && nf > 0) iv = (float)rsqrt((double)nf * rv / nn);
+                    // n*fvar exactly; 1/sqrt(fvar*rv) = P / sqrt(n*fvar*rv).  int64 -> f64 by
+                    // the 2^52 bit trick (exact below 2^52) instead of the conversion unit.
+                    const long long nf = (long long)P * P * h2 - (long long)h1 * h1;
+                    if (rv > 0.0 && nf > 0) {
+                        const double nfd = __longlong_as_double(0x4330000000000000LL | nf) - 4503599627370496.0;
+                        iv = (float)((double)P * rsqrt(nfd * rv));
+                    }
                 } else {
                     const double fvar = h2 - h1 * h1 / nn;  // kernels.py:67
                     if (rv > 0.0 && fvar > 0.0) iv = (float)rsqrt(fvar * rv);
