@@ -323,7 +323,7 @@ def run_ours(args):
                           enumerate(["zncc_group", "finalize", "warp_smooth", "median", "other"])}
     hbm_stage = bytes_frame * t / (step_ms / 1e3) / 1e9
     roofline = {
-        "bound": "fp32", "kernel": "zncc_group_kernel<21,17>",
+        "bound": "fp32", "kernel": "zncc_group_kernel<21,17>", "plan": runner.pre.plan.info(),
         "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
         "traffic": traffic,
         "traffic_source": traffic_src,

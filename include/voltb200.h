@@ -94,6 +94,10 @@ int vb_motion_plan_set_reference(vb_motion_plan* plan, const float* ref_dev, voi
  * float64 [n][(2r+1)][(2r+1)]). */
 int vb_motion_estimate(vb_motion_plan* plan, const void* frames_dev, int dtype, int64_t n_frames,
                        int subpixel, vb_motion* vectors_dev, double* scores_dev, void* stream);
+/* Work decomposition of the plan: patches, CTA patch groups, the largest
+ * group and its union-window width (diagnostics). */
+int vb_motion_plan_info(const vb_motion_plan* plan, int* n_patches, int* n_groups, int* max_group,
+                        int* max_width);
 int vb_motion_plan_destroy(vb_motion_plan* plan);
 
 /* corrected[t] = frame unchanged if the vector is (0,0), else

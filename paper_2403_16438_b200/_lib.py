@@ -49,6 +49,7 @@ SIGNATURES = {
     "vb_motion_plan_create": (_i32, [C.POINTER(_vp), _i32, _i32, _i32, _i32, _vp, _i32]),
     "vb_motion_plan_set_reference": (_i32, [_vp, _vp, _vp]),
     "vb_motion_estimate": (_i32, [_vp, _vp, _i32, _i64, _i32, _vp, _vp, _vp]),
+    "vb_motion_plan_info": (_i32, [_vp] + [C.POINTER(C.c_int)] * 4),
     "vb_motion_plan_destroy": (_i32, [_vp]),
     "vb_correct_frames": (_i32, [_vp, _i32, _i64, _i32, _i32, _vp, _vp, _vp]),
     "vb_summarize": (_i32, [_vp, _i32, _vp, _i64, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _vp, _vp]),

@@ -193,7 +193,7 @@ static int choose_group_size(const std::vector<int32_t>& o, int patch, int radiu
         const int ctas = std::max(1, std::min(std::min(by_smem, by_regs), 32));
         const double occ = std::min(1.0, ctas / 4.0);
         const double score = lane_eff * occ;
-        if (score > best + 1e-9) {
+        if (score >= best - 1e-9) {  // ties: larger groups (fewer CTAs, less per-group overhead; measured)
             best = score;
             best_g = g;
         }
@@ -292,6 +292,15 @@ int vb_motion_estimate(vb_motion_plan* p, const void* frames_dev, int dtype, int
     if (dtype != VB_U16 && dtype != VB_F32) return fail(VB_EINVAL, "unsupported sample type");
     return launch_motion(p->t, p->h, p->w, p->patch, p->radius, frames_dev, dtype, n_frames, subpixel, vectors_dev,
                          scores_dev, (cudaStream_t)stream);
+}
+
+int vb_motion_plan_info(const vb_motion_plan* p, int* n_patches, int* n_groups, int* max_group, int* max_width) {
+    if (!p) return fail(VB_EINVAL, "null argument");
+    if (n_patches) *n_patches = p->t.n;
+    if (n_groups) *n_groups = p->t.n_groups;
+    if (max_group) *max_group = p->t.max_g;
+    if (max_width) *max_width = p->t.max_wu;
+    return VB_OK;
 }
 
 int vb_motion_plan_destroy(vb_motion_plan* p) {

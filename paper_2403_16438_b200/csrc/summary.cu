@@ -365,26 +365,42 @@ __global__ void __launch_bounds__(kK3Threads, 3) warp_smooth_tma_kernel(K3Args a
         phase ^= 1u;
         const int bx0 = s_box[0], by0 = s_box[1];
         // 2. corrected samples on tile + halo (float32, numpy's order); the
-        //    interior goes straight to the corrected output
-        for (int i = tid; i < EH * EW; i += kK3Threads) {
-            const int ey = i / EW, ex = i - ey * EW;
-            const S_T* ra = sRaw + (s_ra[ey] - by0) * BWB - bx0;
-            const S_T* rc = sRaw + (s_rc[ey] - by0) * BWB - bx0;
-            const int xa = s_xa[ex], xb = s_xb[ex];
-            // u16 -> f32 exactly on the ALU/FMA pipes (no I2F on the conversion unit)
-            auto smp = [](S_T v) -> float {
+        //    interior goes straight to the corrected output.  Warps walk rows,
+        //    lanes own fixed columns (their x taps cached in registers).
+        {
+            constexpr int NCS = (EW + 31) / 32;
+            const int lane = tid & 31, warp = tid >> 5;
+            int xa[NCS], xb[NCS];
+#pragma unroll
+            for (int k = 0; k < NCS; ++k) {
+                const int c = lane + 32 * k;
+                xa[k] = c < EW ? s_xa[c] - bx0 : 0;
+                xb[k] = c < EW ? s_xb[c] - bx0 : 0;
+            }
+            auto smp = [](S_T v) -> float {  // u16 -> f32 exactly on the ALU/FMA pipes
                 if constexpr (U16)
                     return u16_minus(v, 8388608.0f);
                 else
                     return v;
             };
-            const float top = __fadd_rn(__fmul_rn(op.omx, smp(ra[xa])), __fmul_rn(op.fx, smp(ra[xb])));
-            const float bot = __fadd_rn(__fmul_rn(op.omx, smp(rc[xa])), __fmul_rn(op.fx, smp(rc[xb])));
-            const float v = __fadd_rn(__fmul_rn(op.omy, top), __fmul_rn(op.fy, bot));
-            sC[ey * EWP + ex] = (double)v;
-            if (a.corrected && ey >= WR && ey < WR + kTY && ex >= WR && ex < WR + kTX) {
-                const int gy = ty0 + ey - WR, gx = tx0 + ex - WR;
-                if (gy < a.h && gx < a.w) a.corrected[t * hw + (int64_t)gy * a.w + gx] = v;
+            float* corr_base = a.corrected ? a.corrected + t * hw : nullptr;
+            for (int ey = warp; ey < EH; ey += kK3Threads / 32) {
+                const S_T* ra = sRaw + (s_ra[ey] - by0) * BWB;
+                const S_T* rc = sRaw + (s_rc[ey] - by0) * BWB;
+                const int gy = ty0 + ey - WR;
+                const bool row_out = corr_base && ey >= WR && ey < WR + kTY && gy < a.h;
+#pragma unroll
+                for (int k = 0; k < NCS; ++k) {
+                    const int c = lane + 32 * k;
+                    if (c < EW) {
+                        const float top = __fadd_rn(__fmul_rn(op.omx, smp(ra[xa[k]])), __fmul_rn(op.fx, smp(ra[xb[k]])));
+                        const float bot = __fadd_rn(__fmul_rn(op.omx, smp(rc[xa[k]])), __fmul_rn(op.fx, smp(rc[xb[k]])));
+                        const float v = __fadd_rn(__fmul_rn(op.omy, top), __fmul_rn(op.fy, bot));
+                        sC[ey * EWP + c] = (double)v;
+                        const int gx = tx0 + c - WR;
+                        if (row_out && c >= WR && c < WR + kTX && gx < a.w) corr_base[(int64_t)gy * a.w + gx] = v;
+                    }
+                }
             }
         }
         __syncthreads();

@@ -169,6 +169,12 @@ class MotionPlan:
                   int(subpixel), vec.data_ptr(), D.ptr(sc), D.stream_handle())
         return vec, sc
 
+    def info(self) -> dict:
+        """Work decomposition (patches, CTA groups, largest group, union width)."""
+        vals = [_lib.C.c_int() for _ in range(4)]
+        _lib.call("vb_motion_plan_info", self._h, *[_lib.C.byref(v) for v in vals])
+        return dict(zip(("patches", "groups", "max_group", "max_width"), (v.value for v in vals)))
+
     def close(self) -> None:
         if getattr(self, "_h", None) is not None and _lib._lib is not None:
             _lib.load().vb_motion_plan_destroy(self._h)
