@@ -508,19 +508,25 @@ constexpr int kK4Pix = 16, kK4Threads = 256;
 // non-negative floats; padding = 0xffffffff never counts).
 template <int VPL>
 __device__ __forceinline__ uint32_t warp_select(const uint32_t (&v)[VPL], uint32_t lo, uint32_t hi, int k) {
-    const uint32_t diff = lo ^ hi;
-    if (diff == 0) return lo;
-    const int nb = 32 - __clz(diff);
-    uint32_t ans = lo & ~((nb == 32) ? 0xffffffffu : ((1u << nb) - 1u));
+    // bisection over u = bits(v) - bits(lo) in [0, hi - lo]: ceil(log2(range))
+    // rounds instead of the highest differing bit of lo ^ hi (values that
+    // straddle a power of two no longer cost a full exponent's worth of rounds)
+    const uint32_t range = hi - lo;
+    if (range == 0) return lo;
+    const int nb = 32 - __clz(range);
+    uint32_t u[VPL];
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) u[i] = v[i] - lo;  // padding (0xffffffff) stays above any candidate
+    uint32_t ans = 0;
     for (int b = nb - 1; b >= 0; --b) {
         const uint32_t cand = ans | (1u << b);
         uint32_t c = 0;
 #pragma unroll
-        for (int i = 0; i < VPL; ++i) c += v[i] < cand ? 1u : 0u;
+        for (int i = 0; i < VPL; ++i) c += u[i] < cand ? 1u : 0u;
         c = __reduce_add_sync(0xffffffffu, c);
         if ((int)c <= k) ans = cand;
     }
-    return ans;
+    return lo + ans;
 }
 
 template <int VPL>
@@ -532,6 +538,7 @@ __global__ void __launch_bounds__(kK4Threads) median_kernel(const float* __restr
     const int cnt = (int)((int64_t)L < n - t0 ? (int64_t)L : n - t0);
     const int64_t p0 = (int64_t)blockIdx.x * kK4Pix;
     const int np = (int)((int64_t)kK4Pix < hw - p0 ? (int64_t)kK4Pix : hw - p0);
+#pragma unroll 8
     for (int i = threadIdx.x; i < cnt * kK4Pix; i += kK4Threads) {
         const int tt = i / kK4Pix, pp = i - tt * kK4Pix;
         sm4[tt * (kK4Pix + 1) + pp] = pp < np ? __ldcs(smoothed + (t0 + tt) * hw + p0 + pp) : 0.f;
