@@ -238,10 +238,21 @@ def run_ours(args):
     from paper_2403_16438_b200 import _device as D
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # BENCH_DIST_BACKEND=gloo (+ ranks sharing one GPU) exercises the N>1 code
+    # path on a single-GPU box: gloo all-reduces are host-mediated, so no
+    # kernel waits on another rank's kernel.  Measurements use NCCL.
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    ngpu = torch.cuda.device_count()
+    if backend == "nccl" and local >= ngpu:
+        raise SystemExit(f"rank {rank}: LOCAL_RANK {local} but only {ngpu} visible GPU(s)")
+    local_dev = local % ngpu
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     cfg = workload(args.config, args.frames)
     L = _lib.load()
     scfg = stage.StageConfig(patch_size=21, search_radius=cfg.radius, subpixel=True, ref_frames=cfg.ref_frames,
@@ -263,7 +274,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local_dev)
     clocks.start()
     time.sleep(0.3)
     L.vb_prof_enable(1)
@@ -342,7 +353,7 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         host = frames.view(torch.int16).cpu().pin_memory()
-        hs = stage.HostStage(cfg.height, cfg.width, scfg, device=local)
+        hs = stage.HostStage(cfg.height, cfg.width, scfg, device=local_dev)
         k = math.ceil(t / cfg.segment_length)
         vec_h = np.empty(t, dtype=_lib.MOTION_DTYPE)
         sp_h = np.empty((k, cfg.height, cfg.width), np.float32)
