@@ -390,7 +390,9 @@ def run_ours(args):
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e_fps = t * world * args.steps / float(et.item())
-        h2d = (t + m) * cfg.height * cfg.width * 2  # rank 0: recording + template head (phase A / all-reduce)
+        # rank 0: the recording (+ the template head uploaded separately for the all-reduce when N > 1;
+        # with N = 1 the template is summed in place from the first resident chunk)
+        h2d = (t + (m if world > 1 else 0)) * cfg.height * cfg.width * 2
         d2h = t * 32 + 2 * k * cfg.height * cfg.width * 4
         e2e = {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "path": "vb_stage_run_host (C ABI), pinned uint16 host input, vectors+summaries to host, "

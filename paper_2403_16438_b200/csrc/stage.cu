@@ -107,7 +107,8 @@ int vb_stage_create(vb_stage** out, const vb_stage_config* cfg) {
     }
     for (auto& wv : st->weights) wv /= tot;
     const int L = cfg->segment_length;
-    int64_t want = cfg->chunk_frames > 0 ? cfg->chunk_frames : 2048;
+    // ~1000-frame chunks: short pipeline fill/drain around the PCIe-bound body
+    int64_t want = cfg->chunk_frames > 0 ? cfg->chunk_frames : 1024;
     st->chunk = std::max<int64_t>(1, (want + L / 2) / L) * L;
     cudaError_t e = cudaStreamCreateWithFlags(&st->s_comp, cudaStreamNonBlocking);
     e = e ? e : cudaStreamCreateWithFlags(&st->s_h2d, cudaStreamNonBlocking);
@@ -218,21 +219,34 @@ int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t 
     }
 
     // ---- phase A: template = mean of the first min(n, M) frames ----
+    // When the template frames lie inside chunk 0 (the usual case), chunk 0 is
+    // uploaded once and the template is summed from it in place; otherwise the
+    // first M frames are streamed through the ring first.
     const int64_t m = st->external_ref ? 0 : std::min<int64_t>(n_frames, c.ref_frames);
+    const bool chunk0_resident = m > 0 && m <= C;
     int rc = VB_OK;
-    for (int64_t f0 = 0, k = 0; f0 < m && rc == VB_OK; f0 += C, ++k) {
-        const int slot = (int)(k & 1);
-        const int64_t nf = std::min<int64_t>(C, m - f0);
-        rc = upload(slot, f0, nf);
-        if (rc) break;
-        VB_CUDA(cudaStreamWaitEvent(st->s_comp, st->ev_h2d[slot], 0));
-        rc = launch_template_sum(st->d_frames[slot], dtype, nf, (int64_t)hw, st->d_tsum, f0 > 0, st->s_comp);
-        if (rc) break;
-        VB_CUDA(cudaEventRecord(st->ev_comp[slot], st->s_comp));
+    if (chunk0_resident) {
+        rc = upload(0, 0, std::min<int64_t>(C, n_frames));
+        if (rc == VB_OK) {
+            VB_CUDA(cudaStreamWaitEvent(st->s_comp, st->ev_h2d[0], 0));
+            rc = launch_template_sum(st->d_frames[0], dtype, m, (int64_t)hw, st->d_tsum, 0, st->s_comp);
+        }
+    } else {
+        for (int64_t f0 = 0, k = 0; f0 < m && rc == VB_OK; f0 += C, ++k) {
+            const int slot = (int)(k & 1);
+            const int64_t nf = std::min<int64_t>(C, m - f0);
+            rc = upload(slot, f0, nf);
+            if (rc) break;
+            VB_CUDA(cudaStreamWaitEvent(st->s_comp, st->ev_h2d[slot], 0));
+            rc = launch_template_sum(st->d_frames[slot], dtype, nf, (int64_t)hw, st->d_tsum, f0 > 0, st->s_comp);
+            if (rc) break;
+            VB_CUDA(cudaEventRecord(st->ev_comp[slot], st->s_comp));
+        }
     }
     if (rc == VB_OK && !st->external_ref) rc = launch_template_finish(st->d_tsum, m, (int64_t)hw, st->d_ref, st->s_comp);
     if (rc == VB_OK) rc = vb_motion_plan_set_reference(st->plan, st->d_ref, st->s_comp);
-    for (int i = 0; i < 2 && rc == VB_OK; ++i) VB_CUDA(cudaEventRecord(st->ev_comp[i], st->s_comp));
+    if (!chunk0_resident)
+        for (int i = 0; i < 2 && rc == VB_OK; ++i) VB_CUDA(cudaEventRecord(st->ev_comp[i], st->s_comp));
 
     // ---- phase B: chunks ----
     const int64_t nchunks = (n_frames + C - 1) / C;
@@ -252,7 +266,7 @@ int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t 
         const int slot = (int)(k & 1);
         const int64_t f0 = k * C, nf = std::min<int64_t>(C, n_frames - f0);
         const int64_t nb = (nf + L - 1) / L;
-        rc = upload(slot, f0, nf);
+        if (!(k == 0 && chunk0_resident)) rc = upload(slot, f0, nf);
         if (rc) break;
         VB_CUDA(cudaStreamWaitEvent(st->s_comp, st->ev_h2d[slot], 0));
         VB_CUDA(cudaStreamWaitEvent(st->s_comp, st->ev_d2h[slot], 0));  // outputs of chunk k-2 drained
