@@ -111,9 +111,8 @@ class ShardedPreprocessor:
         c = self.pre.cfg
         ref = self.template(frames_local, shard, ref_frames)
         self.pre.plan.set_reference(ref)
-        vec, _ = self.pre.plan.estimate(frames_local, c.subpixel)
-        sp, tp = summarize_device(frames_local, c.segment_length, c.sigma, vectors_dev=vec,
-                                  corrected_out=corrected_out)
+        del c, summarize_device
+        vec, sp, tp = self.pre.search_and_summarize(frames_local, corrected_out)
         return DeviceResult(vec, sp, tp, corrected_out, frames_local.shape[0])
 
     def close(self):

@@ -68,15 +68,18 @@ def split_segments(video, segment_length: int = DEFAULT_SEGMENT_LENGTH) -> list[
 
 
 def summarize_device(frames_dev: torch.Tensor, segment_length: int, sigma: float = DEFAULT_SMOOTH_SIGMA,
-                     vectors_dev: torch.Tensor | None = None, corrected_out: torch.Tensor | None = None):
+                     vectors_dev: torch.Tensor | None = None, corrected_out: torch.Tensor | None = None,
+                     spatial_out: torch.Tensor | None = None, temporal_out: torch.Tensor | None = None):
     """Device-resident summaries of a (T,H,W) recording: (spatial, temporal),
     each float32 [ceil(T/L), H, W].  With vectors_dev the motion warp is fused
     (frames are raw) and corrected_out, if given, receives the corrected video."""
     t, h, w = frames_dev.shape
     k = math.ceil(t / segment_length)
     wts, wr = gaussian_weights(sigma)
-    sp = torch.empty((k, h, w), dtype=torch.float32, device=frames_dev.device)
-    tp = torch.empty((k, h, w), dtype=torch.float32, device=frames_dev.device)
+    sp = spatial_out if spatial_out is not None else torch.empty((k, h, w), dtype=torch.float32,
+                                                                 device=frames_dev.device)
+    tp = temporal_out if temporal_out is not None else torch.empty((k, h, w), dtype=torch.float32,
+                                                                   device=frames_dev.device)
     _lib.call("vb_summarize", frames_dev.data_ptr(), D.vb_dtype(frames_dev), D.ptr(vectors_dev), t, h, w,
               segment_length, wts.ctypes.data, wr, D.ptr(corrected_out), sp.data_ptr(), tp.data_ptr(),
               D.stream_handle())
