@@ -198,14 +198,14 @@ __device__ __forceinline__ void box_ready(const ZnccArgs& a, uint64_t* bar, uint
 // input uses float64 sums.  Vertical chains run per (column, 4-row chunk) so
 // every thread has work.  The next frame's box is fetched while this frame's
 // horizontal pass runs.
-template <bool INT>
+template <bool INT, int P_CT>
 __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __grid_constant__ CUtensorMap tmap) {
     using T1 = typename std::conditional<INT, int, double>::type;        // sample / sum of f
     using T2 = typename std::conditional<INT, long long, double>::type;  // sum of f^2
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar;
-    const int P = a.P, S = a.S, SS = S * S, R = (S - 1) / 2;
-    (void)R;
+    const int P = P_CT ? P_CT : a.P;  // compile-time patch: fully unrolled window sums
+    const int S = a.S, SS = S * S;
     const PatchGroup grp = a.groups[blockIdx.x];
     const int G = grp.count, wu = grp.wu, vp = wu | 1;
     const double nn = (double)P * (double)P;
@@ -238,7 +238,9 @@ __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __gri
             };
             T1 s1 = 0;
             T2 s2 = 0;
-            for (int yy = 0; yy < P; ++yy) {
+#pragma unroll
+            for (int yy = 0; yy < (P_CT ? P_CT : 64); ++yy) {
+                if (!P_CT && yy >= P) break;
                 const T1 f = sample(d0 + yy);
                 s1 += f;
                 s2 += (T2)f * (T2)f;
@@ -264,7 +266,9 @@ __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __gri
             const T2* r2 = v2 + dy * vp + col;
             T1 h1 = 0;
             T2 h2 = 0;
-            for (int xx = 0; xx < P; ++xx) {
+#pragma unroll
+            for (int xx = 0; xx < (P_CT ? P_CT : 64); ++xx) {
+                if (!P_CT && xx >= P) break;
                 h1 += r1[xx];
                 h2 += r2[xx];
             }
@@ -579,7 +583,9 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     const int S = 2 * radius + 1, SS = S * S;
     bool fast = false;
     KernelFn fn = pick_kernel(patch, S, &fast);
-    void (*stats_fn)(ZnccArgs, CUtensorMap) = dtype == VB_U16 ? zncc_stats_kernel<true> : zncc_stats_kernel<false>;
+    void (*stats_fn)(ZnccArgs, CUtensorMap) =
+        patch == 21 ? (dtype == VB_U16 ? zncc_stats_kernel<true, 21> : zncc_stats_kernel<false, 21>)
+                    : (dtype == VB_U16 ? zncc_stats_kernel<true, 0> : zncc_stats_kernel<false, 0>);
     SmemPlan sp = zncc_smem(patch, radius, t.max_g, t.max_wu, dtype);
     if (std::max(sp.total, sp.stats_total) > 227 * 1024)
         return fail(VB_EINVAL, "patch group does not fit in shared memory");
