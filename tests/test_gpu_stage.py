@@ -197,3 +197,51 @@ def test_paper_scale_c2_properties(cuda, oracle_mod):
     np.testing.assert_array_equal(tp[1], oracle_mod.temporal_summary(c[1000:2000]))
     assert (tp >= 0).all() and np.isfinite(sp).all()
     pre.close()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,frames", [("c3", 60), ("c5", 24)])
+def test_large_geometries_vs_oracle(cuda, oracle_mod, name, frames):
+    """BASELINE.json configs[2] (512x512, r=12) and configs[4] (1024x1024,
+    r=10) geometries on a short recording: integer shifts and sub-pixel
+    offsets vs the oracle on a frame sample; summaries bit-exact given our
+    corrected frames."""
+    base = synth.CONFIGS[name]
+    cfg = base.with_frames(frames)
+    raw = synth.generate(cfg, cuda)
+    L, m = frames // 2, frames // 3
+    pre = DevicePreprocessor(cfg.height, cfg.width, StageConfig(search_radius=cfg.radius, segment_length=L,
+                                                                 ref_frames=m))
+    corr = torch.empty(raw.shape, dtype=torch.float32, device=cuda)
+    res = pre.run(raw, corrected_out=corr)
+    vec = res.vectors_numpy()
+    host = raw.view(torch.int16).cpu().numpy().view(np.uint16).astype(np.float32)
+    ref_img = oracle_mod.make_reference(host, m)
+    origins = oracle_mod.patch_grid(cfg.height, cfg.width, 21, cfg.radius)
+    for t in (0, frames // 2, frames - 1):
+        dx, dy, sdx, sdy, _ = oracle_mod.estimate_motion(host[t], ref_img, origins, 21, cfg.radius)
+        assert (vec["dx"][t], vec["dy"][t]) == (dx, dy)
+        assert abs(vec["sub_dx"][t] - sdx) <= 1e-3 and abs(vec["sub_dy"][t] - sdy) <= 1e-3
+    c = corr.cpu().numpy()
+    np.testing.assert_array_equal(res.spatial.cpu().numpy()[1], oracle_mod.spatial_summary(c[L:2 * L]))
+    np.testing.assert_array_equal(res.temporal.cpu().numpy()[1], oracle_mod.temporal_summary(c[L:2 * L]))
+    pre.close()
+
+
+@pytest.mark.slow
+def test_streamed_long_recording_c4_geometry(cuda):
+    """configs[3] geometry (512x512, r=10) streamed from pinned host memory in
+    chunks through the C-ABI executor: identical to the device-resident run."""
+    cfg = synth.CONFIGS["c4"].with_frames(3000)
+    raw = synth.generate(cfg, cuda)
+    sc = StageConfig(search_radius=cfg.radius, segment_length=cfg.segment_length, ref_frames=cfg.ref_frames)
+    pre = DevicePreprocessor(cfg.height, cfg.width, sc)
+    res = pre.run(raw)
+    host = raw.view(torch.int16).cpu().pin_memory()
+    hs = HostStage(cfg.height, cfg.width, sc, chunk_frames=1000)
+    vec, sp, tp, _ = hs.run(host.view(torch.uint16))
+    np.testing.assert_array_equal(vec, res.vectors_numpy())
+    np.testing.assert_array_equal(sp, res.spatial.cpu().numpy())
+    np.testing.assert_array_equal(tp, res.temporal.cpu().numpy())
+    hs.close()
+    pre.close()
