@@ -122,6 +122,14 @@ int vb_summarize(const void* frames_dev, int dtype, const vb_motion* vectors_dev
 int vb_smooth_frames(const void* frames_dev, int dtype, int64_t n_frames, int height, int width,
                      const double* weights, int wradius, float* out_dev, void* stream);
 
+/* Trace extraction (traces.py:23-40): out_dev[r][t] =
+ * float64 mean of frames_dev[t] over ROI r's pixels.  ROIs in CSR form:
+ * roi_ptr_dev[n_rois+1] offsets into roi_idx_dev (flattened y*width+x pixel
+ * indices, row-major like np.nonzero); device pointers. */
+int vb_extract_traces(const float* frames_dev, int64_t n_frames, int height, int width,
+                      const int32_t* roi_ptr_dev, const int32_t* roi_idx_dev, int n_rois, double* out_dev,
+                      void* stream);
+
 /* ---------------- whole stage, host buffers (drop-in boundary) ---------------- */
 typedef struct vb_stage_config {
     int height, width;

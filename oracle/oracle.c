@@ -247,6 +247,17 @@ int or_temporal_summary(const float* frames, int n, int h, int w,
     return 0;
 }
 
+/* traces.py:23-34.  numpy reduces the gathered row with pairwise summation;
+ * the sequential float64 sum differs only at ~1e-15 relative. */
+void or_extract_trace(const float* frames, int t, int h, int w, const int32_t* idx, int n, double* out) {
+    size_t px = (size_t)h * w;
+    for (int k = 0; k < t; k++) {
+        double s = 0.0;
+        for (int i = 0; i < n; i++) s += (double)frames[(size_t)k * px + idx[i]];
+        out[k] = s / (double)n;
+    }
+}
+
 /* ---- whole stage ------------------------------------------------------- */
 
 typedef struct {

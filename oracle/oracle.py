@@ -53,6 +53,7 @@ def lib():
                                     C.c_int, _f64p, C.c_int, C.c_int, _i32p, _f64p, C.c_void_p,
                                     _f32p, _f32p]
         L.or_preprocess.restype = C.c_int
+        L.or_extract_trace.argtypes = [_f32p, C.c_int, C.c_int, C.c_int, _i32p, C.c_int, _f64p]
         _lib = L
     return _lib
 
@@ -185,3 +186,16 @@ def preprocess(frames, patch=21, radius=10, subpixel=True, ref_frames=50,
     if rc != 0:
         raise ValueError("invalid preprocess geometry")
     return dict(dxdy=dxdy, sub_conf=sc, corrected=corr, spatial=sp, temporal=tp)
+
+
+def extract_trace(frames, mask) -> np.ndarray:
+    """traces.py:23-34 (samples only)."""
+    f = _f32(frames)
+    bits = np.asarray(getattr(mask, "bits", mask), dtype=bool)
+    ys, xs = np.nonzero(bits)
+    if len(ys) == 0:
+        raise ValueError("empty ROI mask")
+    idx = np.ascontiguousarray(ys * f.shape[2] + xs, dtype=np.int32)
+    out = np.empty(f.shape[0], np.float64)
+    lib().or_extract_trace(f, f.shape[0], f.shape[1], f.shape[2], idx, len(idx), out)
+    return out

@@ -54,6 +54,7 @@ SIGNATURES = {
     "vb_correct_frames": (_i32, [_vp, _i32, _i64, _i32, _i32, _vp, _vp, _vp]),
     "vb_summarize": (_i32, [_vp, _i32, _vp, _i64, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _vp, _vp]),
     "vb_smooth_frames": (_i32, [_vp, _i32, _i64, _i32, _i32, _vp, _i32, _vp, _vp]),
+    "vb_extract_traces": (_i32, [_vp, _i64, _i32, _i32, _vp, _vp, _i32, _vp, _vp]),
     "vb_stage_create": (_i32, [C.POINTER(_vp), C.POINTER(VbStageConfig)]),
     "vb_stage_set_weights": (_i32, [_vp, _vp, _i32]),
     "vb_stage_run_host": (_i32, [_vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _vp]),

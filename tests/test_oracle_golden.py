@@ -99,3 +99,12 @@ def test_even_median_known_answer(golden, oracle_mod):
 def test_gaussian_impulse(golden, oracle_mod):
     z = golden("summary")
     np.testing.assert_array_equal(oracle_mod.smooth_frame(z["gauss_impulse"]), z["gauss_impulse_out"])
+
+
+def test_traces_match_reference(golden, oracle_mod):
+    """traces.py:23-34 extract_trace on random ROIs (reference pairwise float64
+    mean vs the oracle's sequential sum: <= 1e-12 relative)."""
+    z = golden("traces")
+    for k in range(5):
+        got = oracle_mod.extract_trace(z["video"], z[f"mask{k}"])
+        np.testing.assert_allclose(got, z[f"trace{k}"], rtol=1e-12)
