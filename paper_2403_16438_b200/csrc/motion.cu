@@ -312,17 +312,24 @@ __device__ __forceinline__ void cross_row(const float* __restrict__ reg, int pit
 #pragma unroll
         for (int i = 0; i < S + P - 1; ++i) win[i] = fr[i];
         const float4* trow = reinterpret_cast<const float4*>(trow0 + yy * tp);
+        float tv[(P + 3) / 4 * 4];
 #pragma unroll
         for (int q = 0; q < (P + 3) / 4; ++q) {
             const float4 t4 = __ldg(trow + q);
-            const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
+            tv[4 * q] = t4.x;
+            tv[4 * q + 1] = t4.y;
+            tv[4 * q + 2] = t4.z;
+            tv[4 * q + 3] = t4.w;
+        }
+        // anti-diagonal order (window index i = xx + d ascending): the FMAs
+        // consume window samples in the order their loads were issued, so the
+        // row's LDS latency overlaps the arithmetic (and w[i] is the reused
+        // operand of consecutive FFMAs)
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if (4 * q + k < P) {
+        for (int i = 0; i < S + P - 1; ++i) {
 #pragma unroll
-                    for (int d = 0; d < S; ++d) acc[d] = fmaf(win[4 * q + k + d], tv[k], acc[d]);
-                }
-            }
+            for (int xx = (i - (S - 1) > 0 ? i - (S - 1) : 0); xx <= (i < P - 1 ? i : P - 1); ++xx)
+                acc[i - xx] = fmaf(win[i], tv[xx], acc[i - xx]);
         }
     }
 }
