@@ -130,6 +130,43 @@ int vb_extract_traces(const float* frames_dev, int64_t n_frames, int height, int
                       const int32_t* roi_ptr_dev, const int32_t* roi_idx_dev, int n_rois, double* out_dev,
                       void* stream);
 
+/* ---------------- A17 extensions (opt-in, default off) ----------------
+ * The north-star's shading/background correction and per-pixel temporal
+ * high-pass have NO code in the reference; they
+ * are pinned only to this repo's CPU restatement (oracle/oracle.c
+ * or_shading_gain / or_highpass_summary), never to reference outputs. */
+typedef struct vb_summary_opts {
+    int64_t t_global0;     /* recording index of frames_dev[0] */
+    int64_t t_total;       /* frames in the whole recording (reflect boundary of the high-pass) */
+    int64_t interior_off;  /* first summarised frame (index into frames_dev); t_global0 + interior_off
+                              must be a multiple of segment_length */
+    int64_t n_interior;    /* summarised frames: a multiple of segment_length or running to t_total */
+    int highpass_window;   /* odd N >= 3: the temporal summary is taken over x - mean_N(x) (centred
+                              N-frame moving average of the smoothed frames, "reflect" at 0 and
+                              t_total); frames_dev must hold the N/2-frame halo; 0 or 1 = off */
+    const float* gain_dev; /* [h][w] shading gain, corrected = warped / gain (IEEE f32); NULL = off */
+} vb_summary_opts;
+
+/* vb_summarize over part of a longer recording (time shards, chunks with a
+ * halo) with the opt-in extensions.  vectors_dev indexes frames_dev;
+ * corrected_dev receives only the interior frames.  opts == NULL is
+ * vb_summarize.  Errors: those of vb_summarize, "summary interior must start
+ * on a block boundary", "high-pass window must be odd",
+ * "temporal high-pass halo not in the frame buffer". */
+int vb_summarize_ex(const void* frames_dev, int dtype, const vb_motion* vectors_dev, int64_t n_frames,
+                    int height, int width, int segment_length, const double* weights, int wradius,
+                    const vb_summary_opts* opts, float* corrected_dev, float* spatial_dev,
+                    float* temporal_dev, void* stream);
+/* Shading gain from a template: G = separable float64 Gaussian of ref_dev
+ * (host weights[2*wradius+1], taps -r..r in order, "reflect"), gain_dev =
+ * float32(G / mean(G)) with the mean summed in a fixed order. */
+int vb_shading_gain(const float* ref_dev, int height, int width, const double* weights, int wradius,
+                    float* gain_dev, void* stream);
+/* vb_correct_frames followed by division by gain_dev (NULL = no shading). */
+int vb_correct_frames_ex(const void* frames_dev, int dtype, int64_t n_frames, int height, int width,
+                         const vb_motion* vectors_dev, const float* gain_dev, float* corrected_dev,
+                         void* stream);
+
 /* ---------------- whole stage, host buffers (drop-in boundary) ---------------- */
 typedef struct vb_stage_config {
     int height, width;
@@ -158,6 +195,11 @@ int vb_stage_set_weights(vb_stage* stage, const double* weights, int wradius);
 int vb_stage_run_host(vb_stage* stage, const void* frames_host, int dtype, int64_t n_frames,
                       vb_motion* vectors_host, float* spatial_host, float* temporal_host,
                       float* corrected_host, float* corrected_dev);
+/* A17 (opt-in): temporal high-pass window (odd >= 3; 0 = off) and shading
+ * gain weights (NULL = off; the gain is rebuilt from each run's template).
+ * The executor uploads each chunk with its window/2-frame halo. */
+int vb_stage_set_highpass(vb_stage* stage, int window);
+int vb_stage_set_shading(vb_stage* stage, const double* weights, int wradius);
 /* Number of device kernels the last vb_stage_run_host launched. */
 int64_t vb_stage_last_launches(const vb_stage* stage);
 int vb_stage_destroy(vb_stage* stage);

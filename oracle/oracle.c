@@ -258,6 +258,84 @@ void or_extract_trace(const float* frames, int t, int h, int w, const int32_t* i
     }
 }
 
+/* ---- A17 extensions ------------------------------------------------------
+ * The north-star's shading correction and temporal high-pass have NO code in
+ * the reference; the two functions below are their
+ * DEFINITION (parity unpinned to the reference), restated from
+ * include/voltb200.h vb_shading_gain / vb_summary_opts.highpass_window. */
+
+/* gain = f32(G / mean(G)); G = float64 Gaussian of ref, vertical then
+ * horizontal, taps j = -r..r in order (acc += w[j+r] * x), "reflect";
+ * mean = (sum of 1024 strided partials, in index order) / (h*w). */
+void or_shading_gain(const float* ref, int h, int w, const double* wt, int r, float* gain) {
+    size_t px = (size_t)h * w;
+    double* a = (double*)malloc(sizeof(double) * px);
+    double* g = (double*)malloc(sizeof(double) * px);
+    for (int y = 0; y < h; y++)
+        for (int x = 0; x < w; x++) {
+            double acc = 0.0;
+            for (int j = -r; j <= r; j++) acc += wt[j + r] * (double)ref[(size_t)reflect_index(y + j, h) * w + x];
+            a[(size_t)y * w + x] = acc;
+        }
+    for (int y = 0; y < h; y++)
+        for (int x = 0; x < w; x++) {
+            double acc = 0.0;
+            for (int j = -r; j <= r; j++) acc += wt[j + r] * a[(size_t)y * w + reflect_index(x + j, w)];
+            g[(size_t)y * w + x] = acc;
+        }
+    enum { NP = 1024 };
+    double part[NP];
+    for (int k = 0; k < NP; k++) {
+        double s = 0.0;
+        for (size_t i = (size_t)k; i < px; i += NP) s += g[i];
+        part[k] = s;
+    }
+    double tot = 0.0;
+    for (int k = 0; k < NP; k++) tot += part[k];
+    double mean = tot / (double)px;
+    for (size_t i = 0; i < px; i++) gain[i] = (float)(g[i] / mean);
+    free(a); free(g);
+}
+
+/* Temporal summaries with the high-pass: sm = smoothed frames of the whole
+ * recording (summarize.py:70-73 per frame); for every frame t
+ *   hp[t] = f32( f64(sm[t]) - (sum_{tau=-hh..hh} f64(sm[reflect(t+tau, T)])) * (1/N) ),
+ * N = window = 2*hh+1, the sum taken in tau order; then per block of L frames
+ * max - median of hp (summarize.py:76-92 with hp in place of sm). */
+int or_highpass_summary(const float* corrected, int T, int h, int w, const double* weights, int radius,
+                        int segment_length, int window, float* temporal) {
+    if (T < 1 || segment_length < 2 || window < 3 || window % 2 == 0) return -1;
+    size_t px = (size_t)h * w;
+    int hh = window / 2;
+    double inv_n = 1.0 / (double)window;
+    float* sm = (float*)malloc(sizeof(float) * px * (size_t)T);
+    double* scratch = (double*)malloc(sizeof(double) * px);
+    for (int t = 0; t < T; t++) or_smooth_frame(corrected + (size_t)t * px, h, w, weights, radius, sm + (size_t)t * px, scratch);
+    float* col = (float*)malloc(sizeof(float) * (size_t)segment_length);
+    int nseg = (T + segment_length - 1) / segment_length;
+    for (int s = 0; s < nseg; s++) {
+        int lo = s * segment_length, n = (lo + segment_length < T ? lo + segment_length : T) - lo;
+        if (n < 2) { free(col); free(scratch); free(sm); return -2; }
+        int mid = n / 2;
+        for (size_t i = 0; i < px; i++) {
+            float peak = 0.f;
+            for (int k = 0; k < n; k++) {
+                int t = lo + k;
+                double acc = 0.0;
+                for (int tau = -hh; tau <= hh; tau++) acc += (double)sm[(size_t)reflect_index(t + tau, T) * px + i];
+                float hp = (float)((double)sm[(size_t)t * px + i] - acc * inv_n);
+                col[k] = hp;
+                if (k == 0 || hp > peak) peak = hp;
+            }
+            qsort(col, (size_t)n, sizeof(float), cmp_float);
+            float med = (n % 2) ? col[mid] : (col[mid - 1] + col[mid]) * 0.5f;
+            temporal[(size_t)s * px + i] = peak - med;
+        }
+    }
+    free(col); free(scratch); free(sm);
+    return 0;
+}
+
 /* ---- whole stage ------------------------------------------------------- */
 
 typedef struct {

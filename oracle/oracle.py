@@ -54,6 +54,10 @@ def lib():
                                     _f32p, _f32p]
         L.or_preprocess.restype = C.c_int
         L.or_extract_trace.argtypes = [_f32p, C.c_int, C.c_int, C.c_int, _i32p, C.c_int, _f64p]
+        L.or_shading_gain.argtypes = [_f32p, C.c_int, C.c_int, _f64p, C.c_int, _f32p]
+        L.or_highpass_summary.argtypes = [_f32p, C.c_int, C.c_int, C.c_int, _f64p, C.c_int, C.c_int, C.c_int,
+                                          _f32p]
+        L.or_highpass_summary.restype = C.c_int
         _lib = L
     return _lib
 
@@ -198,4 +202,36 @@ def extract_trace(frames, mask) -> np.ndarray:
     idx = np.ascontiguousarray(ys * f.shape[2] + xs, dtype=np.int32)
     out = np.empty(f.shape[0], np.float64)
     lib().or_extract_trace(f, f.shape[0], f.shape[1], f.shape[2], idx, len(idx), out)
+    return out
+
+
+# ---- A17 extensions (no reference counterpart: parity unpinned; the C code
+# is their definition, mirrored by include/voltb200.h) ----------------------
+
+def shading_weights(sigma: float) -> tuple[np.ndarray, int]:
+    """Gaussian taps for the shading gain: scipy's _gaussian_kernel1d with
+    gaussian_filter's default truncate=4 (radius = int(4 sigma + 0.5))."""
+    radius = int(4.0 * float(sigma) + 0.5)
+    x = np.arange(-radius, radius + 1)
+    phi = np.exp(-0.5 / (sigma * sigma) * x ** 2)
+    return np.ascontiguousarray(phi / phi.sum(), dtype=np.float64), radius
+
+
+def shading_gain(reference, sigma: float) -> np.ndarray:
+    ref = _f32(reference)
+    w, r = shading_weights(sigma)
+    out = np.empty_like(ref)
+    lib().or_shading_gain(ref, ref.shape[0], ref.shape[1], w, r, out)
+    return out
+
+
+def highpass_summary(corrected, segment_length: int, window: int, sigma: float = 3.0) -> np.ndarray:
+    """Temporal summaries [K,H,W] of the whole recording with the high-pass."""
+    f = _f32(corrected)
+    t, h, w = f.shape
+    wts, wr = gaussian_weights(sigma)
+    out = np.empty((-(-t // segment_length), h, w), np.float32)
+    rc = lib().or_highpass_summary(f, t, h, w, wts, wr, segment_length, window, out)
+    if rc != 0:
+        raise ValueError("invalid high-pass summary arguments")
     return out

@@ -34,6 +34,12 @@ class VbStageConfig(C.Structure):
                 ("sigma", C.c_double), ("device", C.c_int), ("chunk_frames", C.c_int64)]
 
 
+class VbSummaryOpts(C.Structure):
+    """vb_summary_opts (include/voltb200.h): recording context + A17 options."""
+    _fields_ = [("t_global0", C.c_int64), ("t_total", C.c_int64), ("interior_off", C.c_int64),
+                ("n_interior", C.c_int64), ("highpass_window", C.c_int), ("gain_dev", C.c_void_p)]
+
+
 _vp = C.c_void_p
 _i32, _i64, _dbl = C.c_int, C.c_int64, C.c_double
 
@@ -55,6 +61,12 @@ SIGNATURES = {
     "vb_summarize": (_i32, [_vp, _i32, _vp, _i64, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _vp, _vp]),
     "vb_smooth_frames": (_i32, [_vp, _i32, _i64, _i32, _i32, _vp, _i32, _vp, _vp]),
     "vb_extract_traces": (_i32, [_vp, _i64, _i32, _i32, _vp, _vp, _i32, _vp, _vp]),
+    "vb_summarize_ex": (_i32, [_vp, _i32, _vp, _i64, _i32, _i32, _i32, _vp, _i32, C.POINTER(VbSummaryOpts),
+                               _vp, _vp, _vp, _vp]),
+    "vb_shading_gain": (_i32, [_vp, _i32, _i32, _vp, _i32, _vp, _vp]),
+    "vb_correct_frames_ex": (_i32, [_vp, _i32, _i64, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "vb_stage_set_highpass": (_i32, [_vp, _i32]),
+    "vb_stage_set_shading": (_i32, [_vp, _vp, _i32]),
     "vb_stage_create": (_i32, [C.POINTER(_vp), C.POINTER(VbStageConfig)]),
     "vb_stage_set_weights": (_i32, [_vp, _vp, _i32]),
     "vb_stage_run_host": (_i32, [_vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _vp]),

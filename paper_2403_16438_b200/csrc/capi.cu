@@ -340,8 +340,59 @@ int vb_make_reference(const void* frames_dev, int dtype, int64_t n_frames, int h
 int vb_correct_frames(const void* frames_dev, int dtype, int64_t n_frames, int height, int width,
                       const vb_motion* vectors_dev, float* corrected_dev, void* stream) {
     if (dtype != VB_U16 && dtype != VB_F32) return fail(VB_EINVAL, "unsupported sample type");
-    return launch_correct(frames_dev, dtype, n_frames, height, width, vectors_dev, corrected_dev,
+    return launch_correct(frames_dev, dtype, n_frames, height, width, vectors_dev, nullptr, corrected_dev,
                           (cudaStream_t)stream);
+}
+
+int vb_correct_frames_ex(const void* frames_dev, int dtype, int64_t n_frames, int height, int width,
+                         const vb_motion* vectors_dev, const float* gain_dev, float* corrected_dev, void* stream) {
+    if (dtype != VB_U16 && dtype != VB_F32) return fail(VB_EINVAL, "unsupported sample type");
+    return launch_correct(frames_dev, dtype, n_frames, height, width, vectors_dev, gain_dev, corrected_dev,
+                          (cudaStream_t)stream);
+}
+
+int vb_shading_gain(const float* ref_dev, int height, int width, const double* weights, int wradius,
+                    float* gain_dev, void* stream) {
+    if (!ref_dev || !weights || !gain_dev || wradius < 0) return fail(VB_EINVAL, "null argument");
+    if (height < 1 || width < 1) return fail(VB_EINVAL, "video dimensions must all be >= 1");
+    return launch_shading_gain(ref_dev, height, width, weights, wradius, gain_dev, (cudaStream_t)stream);
+}
+
+int vb_summarize_ex(const void* frames_dev, int dtype, const vb_motion* vectors_dev, int64_t n_frames, int height,
+                    int width, int segment_length, const double* weights, int wradius, const vb_summary_opts* opts,
+                    float* corrected_dev, float* spatial_dev, float* temporal_dev, void* stream) {
+    if (!opts)
+        return vb_summarize(frames_dev, dtype, vectors_dev, n_frames, height, width, segment_length, weights, wradius,
+                            corrected_dev, spatial_dev, temporal_dev, stream);
+    if (segment_length < 2) return fail(VB_EINVAL, "segment length must be >= 2");
+    if (dtype != VB_U16 && dtype != VB_F32) return fail(VB_EINVAL, "unsupported sample type");
+    if (n_frames < 1) return fail(VB_EINVAL, "video dimensions must all be >= 1");
+    if (!weights || wradius < 0 || !spatial_dev || !temporal_dev) return fail(VB_EINVAL, "null argument");
+    const int64_t L = segment_length, T = opts->t_total;
+    const int64_t g0 = opts->t_global0 + opts->interior_off, g1 = g0 + opts->n_interior;
+    if (opts->t_global0 < 0 || opts->t_global0 + n_frames > T || opts->interior_off < 0 || opts->n_interior < 0 ||
+        opts->interior_off + opts->n_interior > n_frames)
+        return fail(VB_EINVAL, "summary interior outside the frame buffer");
+    if (g0 % L != 0) return fail(VB_EINVAL, "summary interior must start on a block boundary");
+    if (opts->n_interior % L != 0 && g1 != T) return fail(VB_EINVAL, "summary interior must end on a block boundary");
+    if (g1 == T && T % L == 1 && opts->n_interior > 0)  // summarize.py:79-80 on the final block
+        return fail(VB_EINVAL, "temporal summary needs at least 2 frames");
+    const int win = opts->highpass_window;
+    if (win > 1) {
+        if (win % 2 == 0) return fail(VB_EINVAL, "high-pass window must be odd");
+        const int64_t hh = win / 2;
+        if (std::max<int64_t>(0, g0 - hh) < opts->t_global0 || std::min<int64_t>(T, g1 + hh) > opts->t_global0 + n_frames)
+            return fail(VB_EINVAL, "temporal high-pass halo not in the frame buffer");
+    }
+    SummaryOpts o;
+    o.t_global0 = opts->t_global0;
+    o.t_total = T;
+    o.interior_off = opts->interior_off;
+    o.n_interior = opts->n_interior;
+    o.highpass_window = win > 1 ? win : 0;
+    o.gain = opts->gain_dev;
+    return launch_summarize_ex(frames_dev, dtype, vectors_dev, n_frames, height, width, segment_length, weights,
+                               wradius, o, corrected_dev, spatial_dev, temporal_dev, (cudaStream_t)stream);
 }
 
 int vb_summarize(const void* frames_dev, int dtype, const vb_motion* vectors_dev, int64_t n_frames, int height,

@@ -45,6 +45,12 @@ struct vb_stage {
     double* d_tsum = nullptr;
     float* d_ref = nullptr;
     bool external_ref = false;
+    // A17 (opt-in): temporal high-pass window and shading gain weights
+    int hp_window = 0;
+    std::vector<double> shade_w;
+    int shade_r = 0;
+    float* d_gain = nullptr;
+    int64_t cap = 0;  // frames per ring slot (chunk + high-pass halo)
     cudaEvent_t ev_h2d[2]{}, ev_comp[2]{}, ev_d2h[2]{};
     int64_t last_launches = 0;
 };
@@ -68,6 +74,7 @@ static void stage_free_buffers(vb_stage* st) {
         st->d_sp[i] = st->d_tp[i] = st->d_corr[i] = nullptr;
     }
     st->esz = 0;
+    st->cap = 0;
 }
 
 extern "C" {
@@ -149,6 +156,33 @@ int vb_stage_set_reference(vb_stage* st, const float* ref_dev) {
     return VB_OK;
 }
 
+int vb_stage_set_highpass(vb_stage* st, int window) {
+    if (!st) return fail(VB_EINVAL, "null argument");
+    if (window > 1 && window % 2 == 0) return fail(VB_EINVAL, "high-pass window must be odd");
+    if (window / 2 > 512) return fail(VB_EINVAL, "high-pass window too long (max 1025 frames)");
+    if (window > 1 && st->cfg.segment_length > 1024)
+        return fail(VB_EINVAL, "temporal high-pass needs segment_length <= 1024");
+    st->hp_window = window > 1 ? window : 0;
+    return VB_OK;
+}
+
+int vb_stage_set_shading(vb_stage* st, const double* weights, int wradius) {
+    if (!st) return fail(VB_EINVAL, "null argument");
+    if (!weights) {
+        st->shade_w.clear();
+        st->shade_r = 0;
+        return VB_OK;
+    }
+    if (wradius < 0) return fail(VB_EINVAL, "null argument");
+    st->shade_w.assign(weights, weights + 2 * wradius + 1);
+    st->shade_r = wradius;
+    if (!st->d_gain) {
+        VB_CUDA(cudaSetDevice(st->cfg.device));
+        VB_CUDA(cudaMalloc(&st->d_gain, (size_t)st->cfg.height * st->cfg.width * sizeof(float)));
+    }
+    return VB_OK;
+}
+
 int64_t vb_stage_last_launches(const vb_stage* st) { return st ? st->last_launches : 0; }
 
 int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t n_frames, vb_motion* vectors_host,
@@ -165,6 +199,9 @@ int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t 
     const size_t esz = dtype == VB_U16 ? 2 : 4;
     const int64_t C = st->chunk;
     const int64_t cblk = C / L;
+    const int64_t hh = st->hp_window / 2;  // high-pass halo per side (0 = off)
+    const int64_t cap = C + 2 * hh;
+    const bool shade = !st->shade_w.empty();
 
     cudaPointerAttributes attr;
     bool pinned = cudaPointerGetAttributes(&attr, frames_host) == cudaSuccess && attr.type == cudaMemoryTypeHost;
@@ -172,13 +209,13 @@ int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t 
 
     // (re)allocate the two-slot ring
     const bool ring_corr = corrected_host && !corrected_dev;  // corrected chunks need ring buffers
-    if (st->esz != esz || (ring_corr && !st->d_corr[0]) || (corrected_host && !st->h_corr[0]) ||
+    if (st->esz != esz || st->cap < cap || (ring_corr && !st->d_corr[0]) || (corrected_host && !st->h_corr[0]) ||
         (!pinned && !st->h_stage[0])) {
         stage_free_buffers(st);
         cudaError_t e = cudaSuccess;
         for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
-            e = cudaMalloc(&st->d_frames[i], (size_t)C * hw * esz);
-            e = e ? e : cudaMalloc(&st->d_vec[i], (size_t)C * sizeof(vb_motion));
+            e = cudaMalloc(&st->d_frames[i], (size_t)cap * hw * esz);
+            e = e ? e : cudaMalloc(&st->d_vec[i], (size_t)cap * sizeof(vb_motion));
             e = e ? e : cudaMalloc(&st->d_sp[i], (size_t)cblk * hw * sizeof(float));
             e = e ? e : cudaMalloc(&st->d_tp[i], (size_t)cblk * hw * sizeof(float));
             if (ring_corr) e = e ? e : cudaMalloc(&st->d_corr[i], (size_t)C * hw * sizeof(float));
@@ -187,14 +224,20 @@ int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t 
             e = e ? e : cudaHostAlloc(&st->h_tp[i], (size_t)cblk * hw * sizeof(float), cudaHostAllocDefault);
             if (corrected_host)
                 e = e ? e : cudaHostAlloc(&st->h_corr[i], (size_t)C * hw * sizeof(float), cudaHostAllocDefault);
-            if (!pinned) e = e ? e : cudaHostAlloc(&st->h_stage[i], (size_t)C * hw * esz, cudaHostAllocDefault);
+            if (!pinned) e = e ? e : cudaHostAlloc(&st->h_stage[i], (size_t)cap * hw * esz, cudaHostAllocDefault);
         }
         if (e != cudaSuccess) {
             stage_free_buffers(st);
             return cuda_fail(e, "vb_stage_run_host allocation");
         }
         st->esz = esz;
+        st->cap = cap;
     }
+    // chunk k covers frames [k*C, k*C + nf); its slot holds them plus the
+    // high-pass halo [a0, a1) (recomputed motion for the halo frames)
+    auto avail = [&](int64_t f0, int64_t nf) {
+        return std::make_pair(std::max<int64_t>(0, f0 - hh), std::min<int64_t>(n_frames, f0 + nf + hh));
+    };
 
     // host->device copy of frames [f0, f0+nf) into slot
     auto upload = [&](int slot, int64_t f0, int64_t nf) -> int {
@@ -226,7 +269,7 @@ int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t 
     const bool chunk0_resident = m > 0 && m <= C;
     int rc = VB_OK;
     if (chunk0_resident) {
-        rc = upload(0, 0, std::min<int64_t>(C, n_frames));
+        rc = upload(0, 0, avail(0, std::min<int64_t>(C, n_frames)).second);
         if (rc == VB_OK) {
             VB_CUDA(cudaStreamWaitEvent(st->s_comp, st->ev_h2d[0], 0));
             rc = launch_template_sum(st->d_frames[0], dtype, m, (int64_t)hw, st->d_tsum, 0, st->s_comp);
@@ -245,6 +288,9 @@ int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t 
     }
     if (rc == VB_OK && !st->external_ref) rc = launch_template_finish(st->d_tsum, m, (int64_t)hw, st->d_ref, st->s_comp);
     if (rc == VB_OK) rc = vb_motion_plan_set_reference(st->plan, st->d_ref, st->s_comp);
+    if (rc == VB_OK && shade)
+        rc = launch_shading_gain(st->d_ref, c.height, c.width, st->shade_w.data(), st->shade_r, st->d_gain,
+                                 st->s_comp);
     if (!chunk0_resident)
         for (int i = 0; i < 2 && rc == VB_OK; ++i) VB_CUDA(cudaEventRecord(st->ev_comp[i], st->s_comp));
 
@@ -266,20 +312,28 @@ int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t 
         const int slot = (int)(k & 1);
         const int64_t f0 = k * C, nf = std::min<int64_t>(C, n_frames - f0);
         const int64_t nb = (nf + L - 1) / L;
-        if (!(k == 0 && chunk0_resident)) rc = upload(slot, f0, nf);
+        const auto [a0, a1] = avail(f0, nf);
+        if (!(k == 0 && chunk0_resident)) rc = upload(slot, a0, a1 - a0);
         if (rc) break;
         VB_CUDA(cudaStreamWaitEvent(st->s_comp, st->ev_h2d[slot], 0));
         VB_CUDA(cudaStreamWaitEvent(st->s_comp, st->ev_d2h[slot], 0));  // outputs of chunk k-2 drained
-        rc = vb_motion_estimate(st->plan, st->d_frames[slot], dtype, nf, c.subpixel, st->d_vec[slot], nullptr,
+        rc = vb_motion_estimate(st->plan, st->d_frames[slot], dtype, a1 - a0, c.subpixel, st->d_vec[slot], nullptr,
                                 st->s_comp);
         if (rc) break;
         float* corr = corrected_dev ? corrected_dev + (size_t)f0 * hw : (corrected_host ? st->d_corr[slot] : nullptr);
-        rc = launch_summarize(st->d_frames[slot], dtype, st->d_vec[slot], nf, c.height, c.width, L,
-                              st->weights.data(), st->wradius, corr, st->d_sp[slot], st->d_tp[slot], st->s_comp);
+        SummaryOpts so;
+        so.t_global0 = a0;
+        so.t_total = n_frames;
+        so.interior_off = f0 - a0;
+        so.n_interior = nf;
+        so.highpass_window = st->hp_window;
+        so.gain = shade ? st->d_gain : nullptr;
+        rc = launch_summarize_ex(st->d_frames[slot], dtype, st->d_vec[slot], a1 - a0, c.height, c.width, L,
+                                 st->weights.data(), st->wradius, so, corr, st->d_sp[slot], st->d_tp[slot], st->s_comp);
         if (rc) break;
         VB_CUDA(cudaEventRecord(st->ev_comp[slot], st->s_comp));
         VB_CUDA(cudaStreamWaitEvent(st->s_d2h, st->ev_comp[slot], 0));
-        VB_CUDA(cudaMemcpyAsync(st->h_vec[slot], st->d_vec[slot], (size_t)nf * sizeof(vb_motion),
+        VB_CUDA(cudaMemcpyAsync(st->h_vec[slot], st->d_vec[slot] + (f0 - a0), (size_t)nf * sizeof(vb_motion),
                                 cudaMemcpyDeviceToHost, st->s_d2h));
         VB_CUDA(cudaMemcpyAsync(st->h_sp[slot], st->d_sp[slot], (size_t)nb * hw * sizeof(float),
                                 cudaMemcpyDeviceToHost, st->s_d2h));
@@ -310,6 +364,7 @@ int vb_stage_destroy(vb_stage* st) {
     vb_motion_plan_destroy(st->plan);
     cudaFree(st->d_tsum);
     cudaFree(st->d_ref);
+    cudaFree(st->d_gain);
     for (int i = 0; i < 2; ++i) {
         if (st->ev_h2d[i]) cudaEventDestroy(st->ev_h2d[i]);
         if (st->ev_comp[i]) cudaEventDestroy(st->ev_comp[i]);

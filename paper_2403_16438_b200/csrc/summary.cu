@@ -88,24 +88,28 @@ __device__ __forceinline__ float warp_sample(const void* f, int dtype, int64_t b
     return __fadd_rn(__fmul_rn(op.omy, top), __fmul_rn(op.fy, bot));
 }
 
+// gain (A17 shading correction, opt-in): corrected = warped / gain[y][x]
+// (IEEE float32 division); null = off.
 __global__ void correct_kernel(const void* __restrict__ frames, int dtype, int64_t n, int h, int w,
-                               const vb_motion* __restrict__ vec, float* __restrict__ out) {
+                               const vb_motion* __restrict__ vec, const float* __restrict__ gain,
+                               float* __restrict__ out) {
     const int64_t hw = (int64_t)h * w;
     for (int64_t t = blockIdx.y; t < n; t += gridDim.y) {
         const WarpOp op = make_warp(vec, t);
         for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hw; i += (int64_t)gridDim.x * blockDim.x) {
             const int y = (int)(i / w), x = (int)(i - (int64_t)y * w);
-            out[t * hw + i] = warp_sample(frames, dtype, t * hw, h, w, op, y, x);
+            const float v = warp_sample(frames, dtype, t * hw, h, w, op, y, x);
+            out[t * hw + i] = gain ? __fdiv_rn(v, __ldg(gain + i)) : v;
         }
     }
 }
 
-int launch_correct(const void* frames, int dtype, int64_t n, int h, int w, const vb_motion* vec, float* out,
-                   cudaStream_t s) {
+int launch_correct(const void* frames, int dtype, int64_t n, int h, int w, const vb_motion* vec,
+                   const float* gain, float* out, cudaStream_t s) {
     if (n <= 0) return VB_OK;
     const int64_t hw = (int64_t)h * w;
     dim3 grid((unsigned)std::min<int64_t>((hw + 255) / 256, 64), (unsigned)std::min<int64_t>(n, 65535));
-    correct_kernel<<<grid, 256, 0, s>>>(frames, dtype, n, h, w, vec, out);
+    correct_kernel<<<grid, 256, 0, s>>>(frames, dtype, n, h, w, vec, gain, out);
     VB_LAUNCHED();
     return VB_OK;
 }
@@ -127,6 +131,7 @@ struct K3Args {
     Weights wt;
     float* corrected;  // [n][h][w] or null
     float* smoothed;   // [n][h][w]
+    const float* gain; // [h][w] shading gain (A17, opt-in): corrected = warped / gain; null = off
 };
 
 // scipy correlate1d symmetric kernel: o = x0*w0; for j=-r..-1: o += (x[j]+x[-j])*w[j]
@@ -180,6 +185,7 @@ __global__ void __launch_bounds__(kK3Threads, 3) warp_smooth_kernel(K3Args a) {
     __shared__ double s_w[2 * kMaxWR + 1];
     __shared__ int s_ra[kTY + 2 * kMaxWR], s_rc[kTY + 2 * kMaxWR];
     __shared__ int s_xa[kTX + 2 * kMaxWR], s_xb[kTX + 2 * kMaxWR];
+    __shared__ int s_gy[kTY + 2 * kMaxWR], s_gx[kTX + 2 * kMaxWR];  // reflected output coordinates
     __shared__ int s_box[4];
     const int tid = threadIdx.x;
     if (tid < 2 * wr + 1) s_w[tid] = a.wt.w[tid];
@@ -196,6 +202,7 @@ __global__ void __launch_bounds__(kK3Threads, 3) warp_smooth_kernel(K3Args a) {
             if (i < EH) {
                 const int y = reflect_index(ty0 - wr + i, a.h);
                 const int ya = clampi(y - op.iy, 0, a.h - 1), yc = clampi(y - op.iy - 1, 0, a.h - 1);
+                s_gy[i] = y;
                 s_ra[i] = ya;
                 s_rc[i] = yc;
                 atomicMin(&s_box[0], min(ya, yc));
@@ -204,6 +211,7 @@ __global__ void __launch_bounds__(kK3Threads, 3) warp_smooth_kernel(K3Args a) {
                 const int e = i - EH;
                 const int x = reflect_index(tx0 - wr + e, a.w);
                 const int xa = clampi(x - op.ix, 0, a.w - 1), xb = clampi(x - op.ix - 1, 0, a.w - 1);
+                s_gx[e] = x;
                 s_xa[e] = xa;
                 s_xb[e] = xb;
                 atomicMin(&s_box[2], min(xa, xb));
@@ -228,7 +236,9 @@ __global__ void __launch_bounds__(kK3Threads, 3) warp_smooth_kernel(K3Args a) {
             const int xa = s_xa[ex], xb = s_xb[ex];
             const float top = __fadd_rn(__fmul_rn(op.omx, ra[xa]), __fmul_rn(op.fx, ra[xb]));
             const float bot = __fadd_rn(__fmul_rn(op.omx, rc[xa]), __fmul_rn(op.fx, rc[xb]));
-            sC[ey * EWP + ex] = (double)__fadd_rn(__fmul_rn(op.omy, top), __fmul_rn(op.fy, bot));
+            float v = __fadd_rn(__fmul_rn(op.omy, top), __fmul_rn(op.fy, bot));
+            if (a.gain) v = __fdiv_rn(v, __ldg(a.gain + (int64_t)s_gy[ey] * a.w + s_gx[ex]));
+            sC[ey * EWP + ex] = (double)v;
         }
         __syncthreads();
         // 4. corrected output (interior) and the H (vertical) pass, rounded to f32
@@ -300,7 +310,7 @@ __device__ __forceinline__ void src_span(int lo, int hi, int n, int i0, int& a0,
 // thread issues the next frame's box (16-byte aligned start, zero-filled out
 // of bounds) as soon as the current box has been consumed, so the global
 // latency overlaps the two float64 passes.
-template <int WR, bool U16>
+template <int WR, bool U16, bool SHADE>
 __global__ void __launch_bounds__(kK3Threads, 3) warp_smooth_tma_kernel(K3Args a, const __grid_constant__ CUtensorMap tmap) {
     constexpr int EH = kTY + 2 * WR, EW = kTX + 2 * WR, EWP = EW | 1;
     constexpr int ALN = U16 ? 8 : 4;                                   // 16-byte alignment in samples
@@ -313,6 +323,7 @@ __global__ void __launch_bounds__(kK3Threads, 3) warp_smooth_tma_kernel(K3Args a
     double* sV = sC + (size_t)EH * EWP;                                                // [kTY][EWP]
     __shared__ double s_w[WR + 1];
     __shared__ int s_ra[EH], s_rc[EH], s_xa[EW], s_xb[EW];
+    __shared__ int s_gy[SHADE ? EH : 1], s_gx[SHADE ? EW : 1];  // reflected output coordinates (gain lookups)
     __shared__ int s_box[2];
     __shared__ __align__(8) uint64_t bar;
     const int tid = threadIdx.x;
@@ -351,11 +362,13 @@ __global__ void __launch_bounds__(kK3Threads, 3) warp_smooth_tma_kernel(K3Args a
         for (int i = tid; i < EH + EW; i += kK3Threads) {
             if (i < EH) {
                 const int y = reflect_index(ty0 - WR + i, a.h);
+                if constexpr (SHADE) s_gy[i] = y;
                 s_ra[i] = clampi(y - op.iy, 0, a.h - 1);
                 s_rc[i] = clampi(y - op.iy - 1, 0, a.h - 1);
             } else {
                 const int e = i - EH;
                 const int x = reflect_index(tx0 - WR + e, a.w);
+                if constexpr (SHADE) s_gx[e] = x;
                 s_xa[e] = clampi(x - op.ix, 0, a.w - 1);
                 s_xb[e] = clampi(x - op.ix - 1, 0, a.w - 1);
             }
@@ -370,12 +383,13 @@ __global__ void __launch_bounds__(kK3Threads, 3) warp_smooth_tma_kernel(K3Args a
         {
             constexpr int NCS = (EW + 31) / 32;
             const int lane = tid & 31, warp = tid >> 5;
-            int xa[NCS], xb[NCS];
+            int xa[NCS], xb[NCS], gxs[NCS];
 #pragma unroll
             for (int k = 0; k < NCS; ++k) {
                 const int c = lane + 32 * k;
                 xa[k] = c < EW ? s_xa[c] - bx0 : 0;
                 xb[k] = c < EW ? s_xb[c] - bx0 : 0;
+                if constexpr (SHADE) gxs[k] = c < EW ? s_gx[c] : 0;
             }
             auto smp = [](S_T v) -> float {  // u16 -> f32 exactly on the ALU/FMA pipes
                 if constexpr (U16)
@@ -389,13 +403,15 @@ __global__ void __launch_bounds__(kK3Threads, 3) warp_smooth_tma_kernel(K3Args a
                 const S_T* rc = sRaw + (s_rc[ey] - by0) * BWB;
                 const int gy = ty0 + ey - WR;
                 const bool row_out = corr_base && ey >= WR && ey < WR + kTY && gy < a.h;
+                const float* grow = SHADE ? a.gain + (int64_t)s_gy[ey] * a.w : nullptr;
 #pragma unroll
                 for (int k = 0; k < NCS; ++k) {
                     const int c = lane + 32 * k;
                     if (c < EW) {
                         const float top = __fadd_rn(__fmul_rn(op.omx, smp(ra[xa[k]])), __fmul_rn(op.fx, smp(ra[xb[k]])));
                         const float bot = __fadd_rn(__fmul_rn(op.omx, smp(rc[xa[k]])), __fmul_rn(op.fx, smp(rc[xb[k]])));
-                        const float v = __fadd_rn(__fmul_rn(op.omy, top), __fmul_rn(op.fy, bot));
+                        float v = __fadd_rn(__fmul_rn(op.omy, top), __fmul_rn(op.fy, bot));
+                        if constexpr (SHADE) v = __fdiv_rn(v, __ldg(grow + gxs[k]));
                         sC[ey * EWP + c] = (double)v;
                         const int gx = tx0 + c - WR;
                         if (row_out && c >= WR && c < WR + kTX && gx < a.w) corr_base[(int64_t)gy * a.w + gx] = v;
@@ -466,7 +482,7 @@ static size_t k3_tma_smem_bytes() {
 template <int WR, bool U16>
 static int launch_k3_tma(const CUtensorMap& tmap, K3Args a, int64_t n, int h, int w, cudaStream_t s) {
     const size_t smem = k3_tma_smem_bytes<WR, U16>();
-    auto kern = warp_smooth_tma_kernel<WR, U16>;
+    auto kern = a.gain ? warp_smooth_tma_kernel<WR, U16, true> : warp_smooth_tma_kernel<WR, U16, false>;
     VB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -503,20 +519,48 @@ __global__ void block_mean_kernel(const float* __restrict__ frames, int64_t n, i
 
 // ------------------------------------------------------------------ K4
 constexpr int kK4Pix = 16, kK4Threads = 256;
+constexpr int kMaxHalfWindow = 512;  // high-pass window N = 2*hh+1 <= 1025 frames
 
-// k-th smallest (0-based) of the warp's values (uint32 patterns of
-// non-negative floats; padding = 0xffffffff never counts).
+// Order-preserving uint32 key of a float32 (total order, -0 < +0): selection
+// works on keys, so the (opt-in, A17) high-passed stacks may hold negatives.
+__device__ __forceinline__ uint32_t fkey(float f) {
+    const uint32_t u = __float_as_uint(f);
+    return u ^ ((uint32_t)((int32_t)u >> 31) | 0x80000000u);
+}
+__device__ __forceinline__ float fkey_inv(uint32_t k) {
+    return __uint_as_float((k & 0x80000000u) ? (k ^ 0x80000000u) : ~k);
+}
+
+__host__ __device__ __forceinline__ int64_t reflect64(int64_t i, int64_t n) {
+    const int64_t period = 2 * n;
+    int64_t m = i % period;
+    if (m < 0) m += period;
+    return m >= n ? period - 1 - m : m;
+}
+
+struct K4Args {
+    const float* sm;   // smoothed frames; scratch row r holds recording frame s_lo + r
+    int64_t s_lo;
+    int64_t g0;        // recording index of the first block's first frame
+    int64_t n;         // frames summarised (blocks of L from g0; the last may be short)
+    int64_t hw;
+    int L;
+    int hh;            // temporal high-pass half window (0 = off), window N = 2*hh + 1
+    double inv_n;      // float64(1 / N)
+    int64_t t_total;   // recording length: reflect boundary of the temporal filter
+    float* temporal;   // [blocks][hw]
+};
+
+// k-th smallest (0-based) of the warp's keys (padding = 0xffffffff never counts).
 template <int VPL>
 __device__ __forceinline__ uint32_t warp_select(const uint32_t (&v)[VPL], uint32_t lo, uint32_t hi, int k) {
-    // bisection over u = bits(v) - bits(lo) in [0, hi - lo]: ceil(log2(range))
-    // rounds instead of the highest differing bit of lo ^ hi (values that
-    // straddle a power of two no longer cost a full exponent's worth of rounds)
+    // bisection over u = key - lo in [0, hi - lo]: ceil(log2(range)) rounds
     const uint32_t range = hi - lo;
     if (range == 0) return lo;
     const int nb = 32 - __clz(range);
     uint32_t u[VPL];
 #pragma unroll
-    for (int i = 0; i < VPL; ++i) u[i] = v[i] - lo;  // padding (0xffffffff) stays above any candidate
+    for (int i = 0; i < VPL; ++i) u[i] = v[i] - lo;  // padding stays above any candidate
     uint32_t ans = 0;
     for (int b = nb - 1; b >= 0; --b) {
         const uint32_t cand = ans | (1u << b);
@@ -529,148 +573,194 @@ __device__ __forceinline__ uint32_t warp_select(const uint32_t (&v)[VPL], uint32
     return lo + ans;
 }
 
+// max - median over the warp's keys (numpy's midpoint for even counts).
 template <int VPL>
-__global__ void __launch_bounds__(kK4Threads) median_kernel(const float* __restrict__ smoothed, int64_t n,
-                                                             int64_t hw, int L, float* __restrict__ temporal) {
-    extern __shared__ float sm4[];  // [L][kK4Pix + 1]
+__device__ __forceinline__ float max_minus_median(const uint32_t (&v)[VPL], uint32_t lo, uint32_t hi, int cnt) {
+    const int mid = cnt / 2;
+    float med;
+    if (cnt & 1) {
+        med = fkey_inv(warp_select<VPL>(v, lo, hi, mid));
+    } else {
+        const uint32_t a = warp_select<VPL>(v, lo, hi, mid - 1);
+        uint32_t le = 0, above = 0xffffffffu;
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+            le += v[i] <= a ? 1u : 0u;
+            if (v[i] > a) above = min(above, v[i]);
+        }
+        le = __reduce_add_sync(0xffffffffu, le);
+        above = __reduce_min_sync(0xffffffffu, above);
+        const uint32_t b = ((int)le >= mid + 1) ? a : above;
+        med = __fmul_rn(__fadd_rn(fkey_inv(a), fkey_inv(b)), 0.5f);
+    }
+    return __fsub_rn(fkey_inv(hi), med);
+}
+
+// One CTA per (block, 16 consecutive pixels): stage the block's smoothed
+// column (plus the high-pass halo, reflected at the recording ends) in shared
+// memory, one warp per pixel.  Without the high-pass lane l holds frames
+// l, l+32, ...; with it lane l owns the contiguous frames [l*VPL, (l+1)*VPL)
+// and slides a float64 window sum over them (exact for camera-range data, so
+// it equals the direct sum the oracle forms): hp = f32(x - sum * (1/N)).
+template <int VPL, bool HP>
+__global__ void __launch_bounds__(kK4Threads) median_kernel(K4Args a) {
+    extern __shared__ float sm4[];  // [cnt + 2 hh][kK4Pix + 1]
+    constexpr int ST = kK4Pix + 1;
     const int blk = blockIdx.y;
-    const int64_t t0 = (int64_t)blk * L;
-    const int cnt = (int)((int64_t)L < n - t0 ? (int64_t)L : n - t0);
+    const int64_t t0 = a.g0 + (int64_t)blk * a.L;
+    const int cnt = (int)((int64_t)a.L < a.g0 + a.n - t0 ? (int64_t)a.L : a.g0 + a.n - t0);
+    const int hh = HP ? a.hh : 0;
+    const int rows = cnt + 2 * hh;
     const int64_t p0 = (int64_t)blockIdx.x * kK4Pix;
-    const int np = (int)((int64_t)kK4Pix < hw - p0 ? (int64_t)kK4Pix : hw - p0);
+    const int np = (int)((int64_t)kK4Pix < a.hw - p0 ? (int64_t)kK4Pix : a.hw - p0);
 #pragma unroll 8
-    for (int i = threadIdx.x; i < cnt * kK4Pix; i += kK4Threads) {
+    for (int i = threadIdx.x; i < rows * kK4Pix; i += kK4Threads) {
         const int tt = i / kK4Pix, pp = i - tt * kK4Pix;
-        sm4[tt * (kK4Pix + 1) + pp] = pp < np ? __ldcs(smoothed + (t0 + tt) * hw + p0 + pp) : 0.f;
+        int64_t g = t0 - hh + tt;
+        if constexpr (HP) g = reflect64(g, a.t_total);
+        sm4[tt * ST + pp] = pp < np ? __ldcs(a.sm + (g - a.s_lo) * a.hw + p0 + pp) : 0.f;
     }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int mid = cnt / 2;
     for (int pp = warp; pp < np; pp += kK4Threads / 32) {
+        const float* col = sm4 + pp;
         uint32_t v[VPL];
         uint32_t lo = 0xffffffffu, hi = 0u;
+        if constexpr (!HP) {
 #pragma unroll
-        for (int i = 0; i < VPL; ++i) {
-            const int tt = lane + 32 * i;
-            v[i] = tt < cnt ? __float_as_uint(sm4[tt * (kK4Pix + 1) + pp]) : 0xffffffffu;
-            if (tt < cnt) {
-                lo = min(lo, v[i]);
-                hi = max(hi, v[i]);
+            for (int i = 0; i < VPL; ++i) {
+                const int tt = lane + 32 * i;
+                v[i] = tt < cnt ? fkey(col[tt * ST]) : 0xffffffffu;
+                if (tt < cnt) {
+                    lo = min(lo, v[i]);
+                    hi = max(hi, v[i]);
+                }
+            }
+        } else {
+            const int tb = lane * VPL;
+            double acc = 0.0;
+            if (tb < cnt)
+                for (int q = 0; q <= 2 * hh; ++q) acc = __dadd_rn(acc, (double)col[(tb + q) * ST]);
+#pragma unroll
+            for (int i = 0; i < VPL; ++i) {
+                const int tt = tb + i;
+                v[i] = 0xffffffffu;
+                if (tt < cnt) {
+                    const float x = col[(tt + hh) * ST];
+                    const float hp = (float)__dsub_rn((double)x, __dmul_rn(acc, a.inv_n));
+                    v[i] = fkey(hp);
+                    lo = min(lo, v[i]);
+                    hi = max(hi, v[i]);
+                    if (tt + 1 < cnt)
+                        acc = __dadd_rn(__dsub_rn(acc, (double)col[tt * ST]), (double)col[(tt + 2 * hh + 1) * ST]);
+                }
             }
         }
         lo = __reduce_min_sync(0xffffffffu, lo);
         hi = __reduce_max_sync(0xffffffffu, hi);
-        float med;
-        if (cnt & 1) {
-            med = __uint_as_float(warp_select<VPL>(v, lo, hi, mid));
-        } else {
-            const uint32_t a = warp_select<VPL>(v, lo, hi, mid - 1);
-            uint32_t le = 0, above = 0xffffffffu;
-#pragma unroll
-            for (int i = 0; i < VPL; ++i) {
-                le += v[i] <= a ? 1u : 0u;
-                if (v[i] > a) above = min(above, v[i]);
-            }
-            le = __reduce_add_sync(0xffffffffu, le);
-            above = __reduce_min_sync(0xffffffffu, above);
-            const uint32_t b = ((int)le >= mid + 1) ? a : above;
-            med = __fmul_rn(__fadd_rn(__uint_as_float(a), __uint_as_float(b)), 0.5f);
-        }
-        if (lane == 0) temporal[(int64_t)blk * hw + p0 + pp] = __fsub_rn(__uint_as_float(hi), med);
+        const float r = max_minus_median<VPL>(v, lo, hi, cnt);
+        if (lane == 0) a.temporal[(int64_t)blk * a.hw + p0 + pp] = r;
     }
 }
 
-// Fallback for blocks longer than 1024 frames: the column is re-read from
-// global memory (L2) on each bisection step.
-__global__ void median_kernel_long(const float* __restrict__ smoothed, int64_t n, int64_t hw, int L,
-                                   float* __restrict__ temporal) {
+// Fallback for blocks longer than 1024 frames (no high-pass): the column is
+// re-read from global memory (L2) on each bisection step.
+__global__ void median_kernel_long(K4Args a) {
     const int blk = blockIdx.y;
-    const int64_t t0 = (int64_t)blk * L;
-    const int cnt = (int)((int64_t)L < n - t0 ? (int64_t)L : n - t0);
+    const int64_t t0 = a.g0 + (int64_t)blk * a.L;
+    const int cnt = (int)((int64_t)a.L < a.g0 + a.n - t0 ? (int64_t)a.L : a.g0 + a.n - t0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t p = (int64_t)blockIdx.x * (blockDim.x / 32) + warp;
-    if (p >= hw) return;
-    const float* col = smoothed + t0 * hw + p;
+    if (p >= a.hw) return;
+    const float* col = a.sm + (t0 - a.s_lo) * a.hw + p;
     uint32_t lo = 0xffffffffu, hi = 0;
     for (int tt = lane; tt < cnt; tt += 32) {
-        const uint32_t u = __float_as_uint(col[(int64_t)tt * hw]);
+        const uint32_t u = fkey(col[(int64_t)tt * a.hw]);
         lo = min(lo, u);
         hi = max(hi, u);
     }
     lo = __reduce_min_sync(0xffffffffu, lo);
     hi = __reduce_max_sync(0xffffffffu, hi);
     auto select = [&](int k) -> uint32_t {
-        const uint32_t diff = lo ^ hi;
-        if (diff == 0) return lo;
-        const int nb = 32 - __clz(diff);
-        uint32_t ans = lo & ~((nb == 32) ? 0xffffffffu : ((1u << nb) - 1u));
+        const uint32_t range = hi - lo;
+        if (range == 0) return lo;
+        const int nb = 32 - __clz(range);
+        uint32_t ans = 0;
         for (int b = nb - 1; b >= 0; --b) {
             const uint32_t cand = ans | (1u << b);
             uint32_t c = 0;
-            for (int tt = lane; tt < cnt; tt += 32) c += __float_as_uint(col[(int64_t)tt * hw]) < cand ? 1u : 0u;
+            for (int tt = lane; tt < cnt; tt += 32) c += fkey(col[(int64_t)tt * a.hw]) - lo < cand ? 1u : 0u;
             c = __reduce_add_sync(0xffffffffu, c);
             if ((int)c <= k) ans = cand;
         }
-        return ans;
+        return lo + ans;
     };
     const int mid = cnt / 2;
     float med;
     if (cnt & 1) {
-        med = __uint_as_float(select(mid));
+        med = fkey_inv(select(mid));
     } else {
-        const uint32_t a = select(mid - 1);
+        const uint32_t ka = select(mid - 1);
         uint32_t le = 0, above = 0xffffffffu;
         for (int tt = lane; tt < cnt; tt += 32) {
-            const uint32_t u = __float_as_uint(col[(int64_t)tt * hw]);
-            le += u <= a ? 1u : 0u;
-            if (u > a) above = min(above, u);
+            const uint32_t u = fkey(col[(int64_t)tt * a.hw]);
+            le += u <= ka ? 1u : 0u;
+            if (u > ka) above = min(above, u);
         }
         le = __reduce_add_sync(0xffffffffu, le);
         above = __reduce_min_sync(0xffffffffu, above);
-        const uint32_t b = ((int)le >= mid + 1) ? a : above;
-        med = __fmul_rn(__fadd_rn(__uint_as_float(a), __uint_as_float(b)), 0.5f);
+        const uint32_t kb = ((int)le >= mid + 1) ? ka : above;
+        med = __fmul_rn(__fadd_rn(fkey_inv(ka), fkey_inv(kb)), 0.5f);
     }
-    if (lane == 0) temporal[(int64_t)blk * hw + p] = __fsub_rn(__uint_as_float(hi), med);
+    if (lane == 0) a.temporal[(int64_t)blk * a.hw + p] = __fsub_rn(fkey_inv(hi), med);
 }
 
-template <int VPL>
-static int launch_median_vpl(const float* sm, int64_t n, int64_t hw, int L, int nblk, float* temporal,
-                             cudaStream_t s) {
-    const size_t smem = (size_t)L * (kK4Pix + 1) * sizeof(float);
-    VB_CUDA(cudaFuncSetAttribute(median_kernel<VPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    dim3 grid((unsigned)((hw + kK4Pix - 1) / kK4Pix), (unsigned)nblk);
+template <int VPL, bool HP>
+static int launch_median_vpl(const K4Args& a, int nblk, cudaStream_t s) {
+    const size_t smem = (size_t)(a.L + 2 * (HP ? a.hh : 0)) * (kK4Pix + 1) * sizeof(float);
+    VB_CUDA(cudaFuncSetAttribute(median_kernel<VPL, HP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid((unsigned)((a.hw + kK4Pix - 1) / kK4Pix), (unsigned)nblk);
     {
         ProfScope ps(kProfMedian, s);
-        median_kernel<VPL><<<grid, kK4Threads, smem, s>>>(sm, n, hw, L, temporal);
+        median_kernel<VPL, HP><<<grid, kK4Threads, smem, s>>>(a);
     }
     VB_LAUNCHED();
     return VB_OK;
 }
 
-static int launch_median(const float* sm, int64_t n, int64_t hw, int L, int nblk, float* temporal, cudaStream_t s) {
-    const int vpl = (L + 31) / 32;
-    if (vpl <= 1) return launch_median_vpl<1>(sm, n, hw, L, nblk, temporal, s);
-    if (vpl <= 2) return launch_median_vpl<2>(sm, n, hw, L, nblk, temporal, s);
-    if (vpl <= 4) return launch_median_vpl<4>(sm, n, hw, L, nblk, temporal, s);
-    if (vpl <= 8) return launch_median_vpl<8>(sm, n, hw, L, nblk, temporal, s);
-    if (vpl <= 16) return launch_median_vpl<16>(sm, n, hw, L, nblk, temporal, s);
-    if (vpl <= 32) return launch_median_vpl<32>(sm, n, hw, L, nblk, temporal, s);
-    dim3 grid((unsigned)((hw + 3) / 4), (unsigned)nblk);
+template <bool HP>
+static int launch_median_hp(const K4Args& a, int nblk, cudaStream_t s) {
+    const int vpl = (a.L + 31) / 32;
+    if (vpl <= 1) return launch_median_vpl<1, HP>(a, nblk, s);
+    if (vpl <= 2) return launch_median_vpl<2, HP>(a, nblk, s);
+    if (vpl <= 4) return launch_median_vpl<4, HP>(a, nblk, s);
+    if (vpl <= 8) return launch_median_vpl<8, HP>(a, nblk, s);
+    if (vpl <= 16) return launch_median_vpl<16, HP>(a, nblk, s);
+    if (vpl <= 32) return launch_median_vpl<32, HP>(a, nblk, s);
+    if (HP) return fail(VB_EINVAL, "temporal high-pass needs segment_length <= 1024");
+    dim3 grid((unsigned)((a.hw + 3) / 4), (unsigned)nblk);
     {
         ProfScope ps(kProfMedian, s);
-        median_kernel_long<<<grid, 128, 0, s>>>(sm, n, hw, L, temporal);
+        median_kernel_long<<<grid, 128, 0, s>>>(a);
     }
     VB_LAUNCHED();
     return VB_OK;
+}
+
+static int launch_median(const K4Args& a, int nblk, cudaStream_t s) {
+    return a.hh > 0 ? launch_median_hp<true>(a, nblk, s) : launch_median_hp<false>(a, nblk, s);
 }
 
 static int launch_k3(const void* frames, int dtype, const vb_motion* vec, int64_t n, int h, int w,
-                     const double* weights, int wradius, float* corrected, float* smoothed, cudaStream_t s) {
+                     const double* weights, int wradius, const float* gain, float* corrected, float* smoothed,
+                     cudaStream_t s) {
+    if (n <= 0) return VB_OK;
     K3Args a;
     a.dtype = dtype;
     a.h = h;
     a.w = w;
     a.wr = wradius;
+    a.gain = gain;
     for (int i = 0; i < 2 * wradius + 1; ++i) a.wt.w[i] = weights[i];
     static const bool no_tma = getenv("VB_NO_TMA") != nullptr;
     if (wradius == 9 && !no_tma && n <= 0x7fffffff) {
@@ -709,38 +799,58 @@ static int launch_k3(const void* frames, int dtype, const vb_motion* vec, int64_
     return VB_OK;
 }
 
-int launch_summarize(const void* frames, int dtype, const vb_motion* vec, int64_t n, int h, int w, int seg_len,
-                     const double* weights, int wradius, float* corrected, float* spatial, float* temporal,
-                     cudaStream_t s) {
+// Summaries of the blocks of `frames` [ioff, ioff + n) (SummaryOpts in vb.cuh).
+// Batches of whole blocks bound the smoothed scratch to ~4 GB.  Per batch:
+// fused warp (+ shading) + smoothing of the batch's frames -- and, with the
+// temporal high-pass, of the hh-frame halo on either side (reflected at the
+// recording ends; halo frames are not written to `corrected`) -- then the
+// per-block mean and the (high-passed) max - median.
+int launch_summarize_ex(const void* frames, int dtype, const vb_motion* vec, int64_t n_avail, int h, int w,
+                        int seg_len, const double* weights, int wradius, const SummaryOpts& o, float* corrected,
+                        float* spatial, float* temporal, cudaStream_t s) {
+    const int64_t n = o.n_interior;
     if (n <= 0) return VB_OK;
     if (wradius > kMaxWR) return fail(VB_EINVAL, "smoothing radius too large (max 16)");
+    const int hh = o.highpass_window > 1 ? o.highpass_window / 2 : 0;
+    if (hh > kMaxHalfWindow) return fail(VB_EINVAL, "high-pass window too long (max 1025 frames)");
+    if (hh > 0 && seg_len > 1024) return fail(VB_EINVAL, "temporal high-pass needs segment_length <= 1024");
     const int64_t hw = (int64_t)h * w;
+    const size_t esz = dtype == VB_U16 ? 2 : 4;
     const int64_t nblk_total = (n + seg_len - 1) / seg_len;
-    // blocks per batch: bound the smoothed (+ corrected) scratch to ~4 GB
     const size_t blk_bytes = (size_t)seg_len * hw * sizeof(float) * (corrected ? 1 : 2);
     int64_t per = std::max<int64_t>(1, (int64_t)((size_t)4 << 30) / (int64_t)blk_bytes);
     per = std::min(per, nblk_total);
-    const size_t frame_bytes = (size_t)seg_len * per * hw * sizeof(float);
+    const size_t smooth_bytes = (size_t)(seg_len * per + 2 * hh) * hw * sizeof(float);
+    const size_t corr_bytes = (size_t)seg_len * per * hw * sizeof(float);
     float* smoothed = nullptr;
     float* corr_scratch = nullptr;
     keep_pool();
-    VB_CUDA(cudaMallocAsync(&smoothed, frame_bytes, s));
+    VB_CUDA(cudaMallocAsync(&smoothed, smooth_bytes, s));
     if (!corrected) {
-        cudaError_t e = cudaMallocAsync(&corr_scratch, frame_bytes, s);
+        cudaError_t e = cudaMallocAsync(&corr_scratch, corr_bytes, s);
         if (e != cudaSuccess) {
             cudaFreeAsync(smoothed, s);
             return cuda_fail(e, "cudaMallocAsync(corrected scratch)");
         }
     }
-    const size_t esz = dtype == VB_U16 ? 2 : 4;
+    auto at = [&](int64_t g) { return (const char*)frames + (size_t)(g - o.t_global0) * hw * esz; };
+    auto vat = [&](int64_t g) { return vec ? vec + (g - o.t_global0) : nullptr; };
     int rc = VB_OK;
     for (int64_t b0 = 0; b0 < nblk_total && rc == VB_OK; b0 += per) {
         const int nb = (int)std::min(per, nblk_total - b0);
-        const int64_t f0 = b0 * seg_len;
-        const int64_t nf = std::min<int64_t>((int64_t)nb * seg_len, n - f0);
-        float* corr = corrected ? corrected + (size_t)f0 * hw : corr_scratch;
-        rc = launch_k3((const char*)frames + (size_t)f0 * hw * esz, dtype, vec ? vec + f0 : nullptr, nf, h, w, weights,
-                       wradius, corr, smoothed, s);
+        const int64_t gi0 = o.t_global0 + o.interior_off + b0 * seg_len;  // recording frame indices
+        const int64_t nf = std::min<int64_t>((int64_t)nb * seg_len, n - b0 * seg_len);
+        const int64_t gi1 = gi0 + nf;
+        const int64_t sg0 = hh ? std::max<int64_t>(0, gi0 - hh) : gi0;
+        const int64_t sg1 = hh ? std::min<int64_t>(o.t_total, gi1 + hh) : gi1;
+        float* corr = corrected ? corrected + (size_t)(b0 * seg_len) * hw : corr_scratch;
+        rc = launch_k3(at(sg0), dtype, vat(sg0), gi0 - sg0, h, w, weights, wradius, o.gain, nullptr, smoothed, s);
+        if (rc == VB_OK)
+            rc = launch_k3(at(gi0), dtype, vat(gi0), nf, h, w, weights, wradius, o.gain, corr,
+                           smoothed + (size_t)(gi0 - sg0) * hw, s);
+        if (rc == VB_OK)
+            rc = launch_k3(at(gi1), dtype, vat(gi1), sg1 - gi1, h, w, weights, wradius, o.gain, nullptr,
+                           smoothed + (size_t)(gi1 - sg0) * hw, s);
         if (rc) break;
         {
             dim3 grid((unsigned)std::min<int64_t>((hw + 255) / 256, 1024), (unsigned)nb);
@@ -753,11 +863,34 @@ int launch_summarize(const void* frames, int dtype, const vb_motion* vec, int64_
             rc = cuda_fail(e, "block_mean_kernel");
             break;
         }
-        rc = launch_median(smoothed, nf, hw, seg_len, nb, temporal + (size_t)b0 * hw, s);
+        K4Args k4;
+        k4.sm = smoothed;
+        k4.s_lo = sg0;
+        k4.g0 = gi0;
+        k4.n = nf;
+        k4.hw = hw;
+        k4.L = seg_len;
+        k4.hh = hh;
+        k4.inv_n = 1.0 / (double)(2 * hh + 1);
+        k4.t_total = o.t_total;
+        k4.temporal = temporal + (size_t)b0 * hw;
+        rc = launch_median(k4, nb, s);
     }
     cudaFreeAsync(smoothed, s);
     if (corr_scratch) cudaFreeAsync(corr_scratch, s);
     return rc;
+}
+
+int launch_summarize(const void* frames, int dtype, const vb_motion* vec, int64_t n, int h, int w, int seg_len,
+                     const double* weights, int wradius, float* corrected, float* spatial, float* temporal,
+                     cudaStream_t s) {
+    SummaryOpts o;
+    o.t_global0 = 0;
+    o.t_total = n;
+    o.interior_off = 0;
+    o.n_interior = n;
+    return launch_summarize_ex(frames, dtype, vec, n, h, w, seg_len, weights, wradius, o, corrected, spatial,
+                               temporal, s);
 }
 
 // Smoothing only (scipy gaussian_filter on each frame, summarize.py:60-73).
@@ -765,7 +898,86 @@ int launch_smooth(const void* frames, int dtype, int64_t n, int h, int w, const 
                   float* out, cudaStream_t s) {
     if (n <= 0) return VB_OK;
     if (wradius > kMaxWR) return fail(VB_EINVAL, "smoothing radius too large (max 16)");
-    return launch_k3(frames, dtype, nullptr, n, h, w, weights, wradius, nullptr, out, s);
+    return launch_k3(frames, dtype, nullptr, n, h, w, weights, wradius, nullptr, nullptr, out, s);
+}
+
+// ------------------------------------------------------------ A17 shading gain
+// Flat-field gain from the template (opt-in, no reference counterpart):
+// G = separable Gaussian of the template (float64 throughout, taps in order
+// -r..r, "reflect" borders, vertical then horizontal), gain = f32(G / mean(G))
+// with mean(G) summed in a fixed order: 1024 strided float64 partials, then
+// the partials in index order (oracle/oracle.c or_shading_gain restates it).
+__global__ void gain_vpass_kernel(const float* __restrict__ ref, int h, int w, const double* __restrict__ wt, int r,
+                                  double* __restrict__ out) {
+    const int64_t hw = (int64_t)h * w;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hw; i += (int64_t)gridDim.x * blockDim.x) {
+        const int y = (int)(i / w), x = (int)(i - (int64_t)y * w);
+        double acc = 0.0;
+        for (int j = -r; j <= r; ++j)
+            acc = __dadd_rn(acc, __dmul_rn(wt[j + r], (double)ref[(int64_t)reflect_index(y + j, h) * w + x]));
+        out[i] = acc;
+    }
+}
+
+__global__ void gain_hpass_kernel(const double* __restrict__ in, int h, int w, const double* __restrict__ wt, int r,
+                                  double* __restrict__ out) {
+    const int64_t hw = (int64_t)h * w;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hw; i += (int64_t)gridDim.x * blockDim.x) {
+        const int y = (int)(i / w), x = (int)(i - (int64_t)y * w);
+        double acc = 0.0;
+        for (int j = -r; j <= r; ++j)
+            acc = __dadd_rn(acc, __dmul_rn(wt[j + r], in[(int64_t)y * w + reflect_index(x + j, w)]));
+        out[i] = acc;
+    }
+}
+
+constexpr int kGainPartials = 1024;
+
+__global__ void __launch_bounds__(kGainPartials) gain_norm_kernel(const double* __restrict__ g, int64_t hw,
+                                                                   float* __restrict__ gain) {
+    __shared__ double part[kGainPartials];
+    __shared__ double mean;
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < hw; i += kGainPartials) acc = __dadd_rn(acc, g[i]);
+    part[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tot = 0.0;
+        for (int k = 0; k < kGainPartials; ++k) tot = __dadd_rn(tot, part[k]);
+        mean = tot / (double)hw;
+    }
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < hw; i += kGainPartials) gain[i] = (float)(g[i] / mean);
+}
+
+int launch_shading_gain(const float* ref, int h, int w, const double* weights_host, int r, float* gain,
+                        cudaStream_t s) {
+    const int64_t hw = (int64_t)h * w;
+    double *wt = nullptr, *a = nullptr, *b = nullptr;
+    keep_pool();
+    VB_CUDA(cudaMallocAsync(&wt, (size_t)(2 * r + 1) * sizeof(double), s));
+    cudaError_t e = cudaMemcpyAsync(wt, weights_host, (size_t)(2 * r + 1) * sizeof(double), cudaMemcpyHostToDevice, s);
+    e = e ? e : cudaMallocAsync(&a, (size_t)hw * sizeof(double), s);
+    e = e ? e : cudaMallocAsync(&b, (size_t)hw * sizeof(double), s);
+    int rc = VB_OK;
+    if (e != cudaSuccess) {
+        rc = cuda_fail(e, "vb_shading_gain allocation");
+    } else {
+        const unsigned grid = (unsigned)std::min<int64_t>((hw + 255) / 256, 4096);
+        ProfScope ps(kProfOther, s);
+        gain_vpass_kernel<<<grid, 256, 0, s>>>(ref, h, w, wt, r, a);
+        gain_hpass_kernel<<<grid, 256, 0, s>>>(a, h, w, wt, r, b);
+        gain_norm_kernel<<<1, kGainPartials, 0, s>>>(b, hw, gain);
+        launches().fetch_add(3, std::memory_order_relaxed);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) rc = cuda_fail(e, "shading gain kernels");
+    }
+    // the host weights must outlive the async copy
+    cudaStreamSynchronize(s);
+    cudaFreeAsync(wt, s);
+    if (a) cudaFreeAsync(a, s);
+    if (b) cudaFreeAsync(b, s);
+    return rc;
 }
 
 }  // namespace vb

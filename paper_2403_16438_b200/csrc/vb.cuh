@@ -81,10 +81,28 @@ int launch_prep_templates(const float* ref, int h, int w, int patch, const Templ
 int launch_motion(const Templates& t, int h, int w, int patch, int radius, const void* frames, int dtype,
                   int64_t n_frames, int subpixel, vb_motion* vectors, double* scores, cudaStream_t s);
 int launch_correct(const void* frames, int dtype, int64_t n, int h, int w, const vb_motion* vec,
-                   float* out, cudaStream_t s);
+                   const float* gain, float* out, cudaStream_t s);
 int launch_summarize(const void* frames, int dtype, const vb_motion* vec, int64_t n, int h, int w,
                      int seg_len, const double* weights, int wradius, float* corrected, float* spatial,
                      float* temporal, cudaStream_t s);
+// Recording context of a summarize call (vb_summary_opts in voltb200.h):
+// frames[0] is recording frame t_global0; blocks of frames [interior_off,
+// interior_off + n_interior) are summarised; the temporal high-pass (A17,
+// opt-in) reflects at 0 and t_total and reads up to window/2 halo frames on
+// either side of the interior.
+struct SummaryOpts {
+    int64_t t_global0 = 0;
+    int64_t t_total = 0;
+    int64_t interior_off = 0;
+    int64_t n_interior = 0;
+    int highpass_window = 0;
+    const float* gain = nullptr;
+};
+int launch_summarize_ex(const void* frames, int dtype, const vb_motion* vec, int64_t n_avail, int h, int w,
+                        int seg_len, const double* weights, int wradius, const SummaryOpts& o, float* corrected,
+                        float* spatial, float* temporal, cudaStream_t s);
+int launch_shading_gain(const float* ref, int h, int w, const double* weights_host, int r, float* gain,
+                        cudaStream_t s);
 int launch_smooth(const void* frames, int dtype, int64_t n, int h, int w, const double* weights, int wradius,
                   float* out, cudaStream_t s);
 

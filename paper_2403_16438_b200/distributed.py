@@ -45,13 +45,26 @@ def shard_plan(n_frames: int, segment_length: int, world: int, rank: int) -> Sha
     return Shard(rank, world, f0, f1, b0, b1, n_frames)
 
 
-def template_rows(shard: Shard, ref_frames: int) -> tuple[int, int]:
-    """Local frame range of this shard that falls inside the template window [0, M)."""
+def halo_range(shard: Shard, highpass_window: int = 0) -> tuple[int, int]:
+    """Recording frames [lo, hi) a rank must hold: its shard plus, with the
+    opt-in temporal high-pass (A17), the window//2-frame halo on either side
+    (clipped to the recording; the filter reflects at its ends)."""
+    hh = highpass_window // 2 if highpass_window and highpass_window > 1 else 0
+    n = shard.n_total or shard.frame_hi
+    return max(0, shard.frame_lo - hh), min(n, shard.frame_hi + hh)
+
+
+def template_rows(shard: Shard, ref_frames: int, local_lo: int | None = None) -> tuple[int, int]:
+    """Local frame range (frames_local[0] = recording frame local_lo, default
+    the shard start) of this shard's OWN frames inside the template window
+    [0, M) -- halo frames are never counted, so the all-reduced sum counts each
+    template frame once."""
+    base = shard.frame_lo if local_lo is None else local_lo
     lo = max(shard.frame_lo, 0)
     hi = min(shard.frame_hi, ref_frames)
     if hi <= lo:
         return 0, 0
-    return lo - shard.frame_lo, hi - shard.frame_lo
+    return lo - base, hi - base
 
 
 def allreduce_sum_(t: torch.Tensor, group=None) -> torch.Tensor:
@@ -88,13 +101,14 @@ class ShardedPreprocessor:
         self.group = group
         self.height, self.width = height, width
 
-    def template(self, frames_local: torch.Tensor, shard: Shard, ref_frames: int) -> torch.Tensor:
+    def template(self, frames_local: torch.Tensor, shard: Shard, ref_frames: int,
+                 local_lo: int | None = None) -> torch.Tensor:
         from . import _device as D
         from . import _lib
 
         h, w = self.height, self.width
         tsum = torch.zeros((h, w), dtype=torch.float64, device=frames_local.device)
-        lo, hi = template_rows(shard, ref_frames)
+        lo, hi = template_rows(shard, ref_frames, local_lo)
         if hi > lo:
             _lib.call("vb_template_sum", frames_local[lo:hi].data_ptr(), D.vb_dtype(frames_local), hi - lo, h, w,
                       tsum.data_ptr(), 0, D.stream_handle())
@@ -104,15 +118,21 @@ class ShardedPreprocessor:
         _lib.call("vb_template_finish", tsum.data_ptr(), m, h * w, ref.data_ptr(), D.stream_handle())
         return ref
 
-    def run(self, frames_local: torch.Tensor, shard: Shard, ref_frames: int, corrected_out=None):
+    def run(self, frames_local: torch.Tensor, shard: Shard, ref_frames: int, corrected_out=None,
+            local_lo: int | None = None):
+        """frames_local = recording frames [local_lo, local_lo + len) -- the
+        shard, or halo_range(shard, window) with the opt-in high-pass.  Vectors
+        cover every local frame (halo ones are recomputed, not exchanged);
+        summaries and corrected_out cover the shard's own blocks/frames."""
         from .stage import DeviceResult
-        from .summarize import summarize_device
 
-        c = self.pre.cfg
-        ref = self.template(frames_local, shard, ref_frames)
+        base = shard.frame_lo if local_lo is None else local_lo
+        ref = self.template(frames_local, shard, ref_frames, base)
         self.pre.plan.set_reference(ref)
-        del c, summarize_device
-        vec, sp, tp = self.pre.search_and_summarize(frames_local, corrected_out)
+        self.pre.set_shading(ref)
+        vec, sp, tp = self.pre.search_and_summarize(
+            frames_local, corrected_out, t_global0=base, t_total=shard.n_total or shard.frame_hi,
+            interior=(shard.frame_lo - base, shard.frames))
         return DeviceResult(vec, sp, tp, corrected_out, frames_local.shape[0])
 
     def close(self):

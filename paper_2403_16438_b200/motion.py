@@ -18,6 +18,7 @@ import torch
 
 from . import _device as D
 from . import _lib
+from .extensions import shading_gain_device
 from .video import Video
 
 DEFAULT_PATCH_SIZE = 21
@@ -114,6 +115,9 @@ class MotionConfig:
     search_radius: int = DEFAULT_SEARCH_RADIUS
     subpixel: bool = True
     threads: int = 1
+    # A17 (opt-in, no reference counterpart; extensions.py): > 0 divides the
+    # corrected frames by the template's flat-field gain at this sigma
+    shading_sigma: float = 0.0
 
 
 @lru_cache(maxsize=8)
@@ -244,11 +248,12 @@ def translate(frame: np.ndarray, dx: float, dy: float) -> np.ndarray:
     return out[0].cpu().numpy()
 
 
-def correct_frames_device(frames_dev: torch.Tensor, vectors_dev: torch.Tensor) -> torch.Tensor:
+def correct_frames_device(frames_dev: torch.Tensor, vectors_dev: torch.Tensor,
+                          gain: torch.Tensor | None = None) -> torch.Tensor:
     t, h, w = frames_dev.shape
     out = torch.empty((t, h, w), dtype=torch.float32, device=frames_dev.device)
-    _lib.call("vb_correct_frames", frames_dev.data_ptr(), D.vb_dtype(frames_dev), t, h, w,
-              vectors_dev.data_ptr(), out.data_ptr(), D.stream_handle())
+    _lib.call("vb_correct_frames_ex", frames_dev.data_ptr(), D.vb_dtype(frames_dev), t, h, w,
+              vectors_dev.data_ptr(), D.ptr(gain), out.data_ptr(), D.stream_handle())
     return out
 
 
@@ -267,7 +272,8 @@ def correct_motion(video, config: MotionConfig | None = None) -> tuple[Video, li
     try:
         plan.set_reference(ref)
         vec, _ = plan.estimate(frames, config.subpixel)
-        corrected = correct_frames_device(frames, vec)
+        gain = shading_gain_device(ref, config.shading_sigma) if config.shading_sigma > 0 else None
+        corrected = correct_frames_device(frames, vec, gain)
         rec = D.motion_to_numpy(vec, v.frames)
         out = corrected.cpu().numpy()
     finally:

@@ -23,6 +23,7 @@ import torch
 from . import _device as D
 from . import _lib
 from . import motion as M
+from .extensions import check_window, shading_gain_device, shading_weights
 from .summarize import DEFAULT_SEGMENT_LENGTH, DEFAULT_SMOOTH_SIGMA, SummaryPair, gaussian_weights, summarize_device
 from .video import Video
 
@@ -35,6 +36,9 @@ class StageConfig:
     ref_frames: int | None = None  # None -> motion.REFERENCE_FRAMES at call time
     segment_length: int = DEFAULT_SEGMENT_LENGTH
     sigma: float = DEFAULT_SMOOTH_SIGMA
+    # A17 extensions (opt-in, default off; no reference counterpart -- extensions.py)
+    highpass_window: int = 0     # odd N: temporal summary over x - mean_N(x)
+    shading_sigma: float = 0.0   # > 0: corrected = warped / flat-field gain of the template
 
 
 @dataclass
@@ -68,6 +72,8 @@ class DevicePreprocessor:
         self.grid = M.PatchGrid.cover(height, width, c.patch_size, margin=c.search_radius)
         self.plan = M.MotionPlan(height, width, self.grid.origins, c.patch_size, c.search_radius)
         self.weights, self.wradius = gaussian_weights(c.sigma)
+        self.window = check_window(c.highpass_window)
+        self.gain = None
 
     def run(self, frames: torch.Tensor, corrected_out: torch.Tensor | None = None,
             vectors_out: torch.Tensor | None = None) -> DeviceResult:
@@ -77,6 +83,7 @@ class DevicePreprocessor:
         m = M.REFERENCE_FRAMES if self.cfg.ref_frames is None else self.cfg.ref_frames
         ref = M.device_reference(frames, m)
         self.plan.set_reference(ref)
+        self.set_shading(ref)
         vec, sp, tp = self.search_and_summarize(frames, corrected_out, vectors_out)
         return DeviceResult(vec, sp, tp, corrected_out, t)
 
@@ -85,8 +92,14 @@ class DevicePreprocessor:
     # already saturated; concurrent kernels only slow each other), so serial.
     overlap_blocks = int(os.environ.get("VB_OVERLAP_BLOCKS", "0"))
 
+    def set_shading(self, ref: torch.Tensor) -> None:
+        """Flat-field gain of this recording's template (A17; no-op when off)."""
+        s = self.cfg.shading_sigma
+        self.gain = shading_gain_device(ref, s) if s and s > 0 else None
+
     def search_and_summarize(self, frames: torch.Tensor, corrected_out: torch.Tensor | None = None,
-                             vectors_out: torch.Tensor | None = None):
+                             vectors_out: torch.Tensor | None = None, t_global0: int = 0,
+                             t_total: int | None = None, interior: tuple[int, int] | None = None):
         """Motion search then fused warp + summaries, pipelined in block-aligned
         chunks over two streams: the search of chunk k+1 (FP32-bound) runs
         while the summaries of chunk k (FP64-bound) do, so the two kernels'
@@ -100,10 +113,14 @@ class DevicePreprocessor:
         sp = torch.empty((k_blocks, self.height, self.width), dtype=torch.float32, device=dev)
         tp = torch.empty_like(sp)
         chunk = L * self.overlap_blocks if self.overlap_blocks > 0 else t
-        if chunk >= t:
+        if interior is not None:
+            k_blocks = math.ceil(interior[1] / L)
+            sp, tp = sp[:k_blocks], tp[:k_blocks]
+        if chunk >= t or self.window or self.gain is not None or interior is not None:
             self.plan.estimate(frames, c.subpixel, out=vec)
             summarize_device(frames, L, c.sigma, vectors_dev=vec, corrected_out=corrected_out,
-                             spatial_out=sp, temporal_out=tp)
+                             spatial_out=sp, temporal_out=tp, highpass_window=self.window, gain=self.gain,
+                             t_global0=t_global0, t_total=t_total, interior=interior)
             return vec, sp, tp
         main = torch.cuda.current_stream(dev)
         if getattr(self, "_side", None) is None:
@@ -170,6 +187,10 @@ class HostStage:
         w, r = gaussian_weights(c.sigma)
         self._w = w
         _lib.call("vb_stage_set_weights", self._h, w.ctypes.data, r)
+        _lib.call("vb_stage_set_highpass", self._h, check_window(c.highpass_window))
+        if c.shading_sigma and c.shading_sigma > 0:
+            self._sw, sr = shading_weights(c.shading_sigma)
+            _lib.call("vb_stage_set_shading", self._h, self._sw.ctypes.data, sr)
         self.height, self.width = height, width
 
     def run(self, frames: np.ndarray, corrected: bool = False):

@@ -15,6 +15,7 @@ import torch
 
 from . import _device as D
 from . import _lib
+from .extensions import check_window
 from .video import Video
 
 DEFAULT_SEGMENT_LENGTH = 50
@@ -69,20 +70,39 @@ def split_segments(video, segment_length: int = DEFAULT_SEGMENT_LENGTH) -> list[
 
 def summarize_device(frames_dev: torch.Tensor, segment_length: int, sigma: float = DEFAULT_SMOOTH_SIGMA,
                      vectors_dev: torch.Tensor | None = None, corrected_out: torch.Tensor | None = None,
-                     spatial_out: torch.Tensor | None = None, temporal_out: torch.Tensor | None = None):
+                     spatial_out: torch.Tensor | None = None, temporal_out: torch.Tensor | None = None, *,
+                     highpass_window: int = 0, gain: torch.Tensor | None = None, t_global0: int = 0,
+                     t_total: int | None = None, interior: tuple[int, int] | None = None):
     """Device-resident summaries of a (T,H,W) recording: (spatial, temporal),
-    each float32 [ceil(T/L), H, W].  With vectors_dev the motion warp is fused
-    (frames are raw) and corrected_out, if given, receives the corrected video."""
+    each float32 [ceil(n/L), H, W].  With vectors_dev the motion warp is fused
+    (frames are raw) and corrected_out, if given, receives the corrected video.
+
+    Recording context (time shards / chunks): frames_dev[0] is recording frame
+    t_global0 of t_total, and only the blocks of frames_dev[interior[0] :
+    interior[0] + interior[1]] are summarised (corrected_out then holds those
+    frames only).  A17 (opt-in, extensions.py): highpass_window = odd N takes
+    the temporal summary over x - mean_N(x) (frames_dev must then include the
+    N/2-frame halo around the interior); gain = shading gain [H,W]."""
     t, h, w = frames_dev.shape
-    k = math.ceil(t / segment_length)
+    window = check_window(highpass_window)
+    ioff, n = interior if interior is not None else (0, t)
+    k = math.ceil(n / segment_length)
     wts, wr = gaussian_weights(sigma)
     sp = spatial_out if spatial_out is not None else torch.empty((k, h, w), dtype=torch.float32,
                                                                  device=frames_dev.device)
     tp = temporal_out if temporal_out is not None else torch.empty((k, h, w), dtype=torch.float32,
                                                                    device=frames_dev.device)
-    _lib.call("vb_summarize", frames_dev.data_ptr(), D.vb_dtype(frames_dev), D.ptr(vectors_dev), t, h, w,
-              segment_length, wts.ctypes.data, wr, D.ptr(corrected_out), sp.data_ptr(), tp.data_ptr(),
-              D.stream_handle())
+    extended = window or gain is not None or t_global0 or interior is not None or (t_total not in (None, t))
+    if not extended:
+        _lib.call("vb_summarize", frames_dev.data_ptr(), D.vb_dtype(frames_dev), D.ptr(vectors_dev), t, h, w,
+                  segment_length, wts.ctypes.data, wr, D.ptr(corrected_out), sp.data_ptr(), tp.data_ptr(),
+                  D.stream_handle())
+        return sp, tp
+    opts = _lib.VbSummaryOpts(int(t_global0), int(t_total if t_total is not None else t_global0 + t), int(ioff),
+                              int(n), int(window), D.ptr(gain))
+    _lib.call("vb_summarize_ex", frames_dev.data_ptr(), D.vb_dtype(frames_dev), D.ptr(vectors_dev), t, h, w,
+              segment_length, wts.ctypes.data, wr, _lib.C.byref(opts), D.ptr(corrected_out), sp.data_ptr(),
+              tp.data_ptr(), D.stream_handle())
     return sp, tp
 
 
@@ -134,13 +154,14 @@ def summarize_segment(segment: TimeSegment, sigma: float = DEFAULT_SMOOTH_SIGMA)
 
 
 def summarize(video, segment_length: int = DEFAULT_SEGMENT_LENGTH,
-              sigma: float = DEFAULT_SMOOTH_SIGMA) -> list[SummaryPair]:
-    """summarize.py:99-102: one SummaryPair per segment (all blocks in one launch)."""
+              sigma: float = DEFAULT_SMOOTH_SIGMA, *, highpass_window: int = 0) -> list[SummaryPair]:
+    """summarize.py:99-102: one SummaryPair per segment (all blocks in one launch).
+    highpass_window (A17, opt-in, default off): see extensions.py."""
     if segment_length < 2:
         raise ValueError("segment length must be >= 2")
     v = Video.wrap(video)
     frames = D.as_device_frames(v.samples)
-    sp, tp = summarize_device(frames, segment_length, sigma)
+    sp, tp = summarize_device(frames, segment_length, sigma, highpass_window=highpass_window)
     sp, tp = sp.cpu().numpy(), tp.cpu().numpy()
     return [SummaryPair(i, sp[i], tp[i]) for i in range(sp.shape[0])]
 
