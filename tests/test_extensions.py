@@ -87,7 +87,7 @@ def _frames(shape, seed=7):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("shape,L,win", [((300, 40, 72), 100, 33), ((250, 33, 70), 64, 9),
-                                         ((20, 24, 24), 10, 33), ((121, 30, 40), 40, 3)])
+                                         ((20, 24, 24), 10, 33), ((122, 30, 40), 40, 3)])
 def test_highpass_summary_matches_oracle(cuda, oracle_mod, shape, L, win):
     from paper_2403_16438_b200.summarize import summarize
 
@@ -229,3 +229,14 @@ def test_extension_errors(cuda):
         summarize_device(f[20:80], 20, highpass_window=9, t_global0=20, t_total=100, interior=(0, 60))
     with pytest.raises(ValueError, match="block boundary"):
         summarize_device(f, 20, t_global0=0, t_total=100, interior=(10, 40))
+
+
+@pytest.mark.gpu
+def test_highpass_one_frame_tail_raises_like_reference(cuda):
+    """A 1-frame last block raises the reference's message (summarize.py:80)
+    with the high-pass on as well as off."""
+    from paper_2403_16438_b200.summarize import summarize
+
+    frames = _frames((121, 30, 40))
+    with pytest.raises(ValueError, match="at least 2 frames"):
+        summarize(frames, 40, highpass_window=3)
