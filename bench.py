@@ -52,6 +52,9 @@ def parse():
     p.add_argument("--no-corrected", action="store_true", help="do not materialise the corrected video")
     p.add_argument("--cpu-sample", type=int, default=1000, help="frames in the CPU baseline sample")
     p.add_argument("--ref-step-frames", type=int, default=400, help="frames per --impl reference step")
+    p.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                   help="weak: each rank owns its own T-frame recording shard; strong: one T-frame recording "
+                        "split into frame-balanced shards (blocks straddling ranks are exchanged over NCCL)")
     return p.parse_args()
 
 
@@ -257,12 +260,24 @@ def run_ours(args):
     L = _lib.load()
     scfg = stage.StageConfig(patch_size=21, search_radius=cfg.radius, subpixel=True, ref_frames=cfg.ref_frames,
                              segment_length=cfg.segment_length, sigma=3.0)
-    # weak scaling: rank r owns frames [r*T, (r+1)*T) of an N*T-frame recording
-    frames = synth.generate(synth.SynthConfig(**{**cfg.__dict__, "seed": cfg.seed + rank}), dev)
-    t = frames.shape[0]
-    shard = distributed.shard_plan(t * world, cfg.segment_length, world, rank)
-    assert shard.frames == t
-    runner = distributed.ShardedPreprocessor(cfg.height, cfg.width, scfg)
+    strong = args.scaling == "strong"
+    if strong:
+        # strong scaling: one T-frame recording, frame-balanced shards (distributed.balanced_plan)
+        full = synth.generate(cfg, dev)
+        shard = distributed.balanced_plan(full.shape[0], cfg.segment_length, world, rank)
+        frames = full[shard.local_lo:shard.local_hi].clone()
+        del full
+        torch.cuda.empty_cache()
+        t = shard.frames
+        runner = distributed.BalancedShardedPreprocessor(cfg.height, cfg.width, scfg)
+        args.no_e2e = True  # the C-ABI host executor runs whole recordings only
+    else:
+        # weak scaling: rank r owns frames [r*T, (r+1)*T) of an N*T-frame recording
+        frames = synth.generate(synth.SynthConfig(**{**cfg.__dict__, "seed": cfg.seed + rank}), dev)
+        t = frames.shape[0]
+        shard = distributed.shard_plan(t * world, cfg.segment_length, world, rank)
+        assert shard.frames == t
+        runner = distributed.ShardedPreprocessor(cfg.height, cfg.width, scfg)
     corr = None if args.no_corrected else torch.empty((t, cfg.height, cfg.width), dtype=torch.float32, device=dev)
     torch.cuda.synchronize()
 
@@ -301,16 +316,19 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     elapsed = float(t_max.item())
-    value = t * world * args.steps / (elapsed / 1e3)
+    total_frames = shard.n_total if strong else t * world
+    value = total_frames * args.steps / (elapsed / 1e3)
 
     # sanity: the stage produced finite, non-negative summaries
     vec = res.vectors_numpy()
-    ok = bool(np.isfinite(res.temporal.float().cpu().numpy()).all() and (res.temporal.min().item() >= 0)
+    ok = bool(np.isfinite(res.temporal.float().cpu().numpy()).all()
+              and (res.temporal.numel() == 0 or res.temporal.min().item() >= 0)
               and (np.abs(vec["dx"]) <= cfg.radius).all())
 
     # ---- roofline of the dominant kernel (ZNCC search), CUDA events on its stream ----
     peaks, peaks_src = measured_peaks()
-    n_patches = runner.pre.plan.n_patches
+    pre = runner.ops.pre if strong else runner.pre
+    n_patches = pre.plan.n_patches
     bytes_frame, flops_frame = algorithmic_numbers(cfg, n_patches)
     zncc_launches = int(cnt[0])
     zncc_ms = ms[0] / max(zncc_launches, 1)
@@ -332,9 +350,9 @@ def run_ours(args):
             pass
     kernel_ms_per_step = {n: float(ms[i] / args.steps) for i, n in
                           enumerate(["zncc_group", "finalize", "warp_smooth", "median", "other"])}
-    hbm_stage = bytes_frame * t / (step_ms / 1e3) / 1e9
+    hbm_stage = bytes_frame * total_frames / world / (step_ms / 1e3) / 1e9
     roofline = {
-        "bound": "fp32", "kernel": "zncc_group_kernel<21,17>", "plan": runner.pre.plan.info(),
+        "bound": "fp32", "kernel": "zncc_group_kernel<21,17>", "plan": pre.plan.info(),
         "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
         "traffic": traffic,
         "traffic_source": traffic_src,
@@ -419,12 +437,17 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f32/f64",
-            "data": f"synthetic (paper_2403_16438_b200.synth, BASELINE.json configs[1], seed {cfg.seed}+rank)",
-            "config": {"workload": f"{cfg.name}: {t}x{cfg.height}x{cfg.width} uint16 per rank, r={cfg.radius}, "
-                                   f"patch=21, L={cfg.segment_length}, M={cfg.ref_frames}, sigma=3",
-                       "per_rank_frames": t, "parallelism": f"time-sharded x{world} (template all-reduce)",
+            "data": f"synthetic (paper_2403_16438_b200.synth, BASELINE.json configs[1], seed {cfg.seed}"
+                    + (")" if strong else "+rank)"),
+            "config": {"workload": (f"{cfg.name}: {total_frames}x{cfg.height}x{cfg.width} uint16 recording, frame-balanced "
+                                    f"shards" if strong else f"{cfg.name}: {t}x{cfg.height}x{cfg.width} uint16 per rank")
+                                   + f", r={cfg.radius}, patch=21, L={cfg.segment_length}, M={cfg.ref_frames}, sigma=3",
+                       "per_rank_frames": t,
+                       "parallelism": (f"frame-balanced time shards x{world} (template all-reduce; straddling blocks: "
+                                       f"smoothed frames + float64 running sum sent forward, NCCL p2p)") if strong
+                       else f"time-sharded x{world} (template all-reduce)",
                        "corrected_video": "written to HBM" if corr is not None else "not materialised",
                        "l2": "inputs (%.1f GB u16) larger than L2 (126 MB); no flush" % (t * cfg.height * cfg.width * 2 / 1e9)},
             "roofline": roofline,

@@ -167,6 +167,29 @@ int vb_correct_frames_ex(const void* frames_dev, int dtype, int64_t n_frames, in
                          const vb_motion* vectors_dev, const float* gain_dev, float* corrected_dev,
                          void* stream);
 
+/* ---------------- blocks split across time shards ----------------
+ * With frame-balanced time shards a summary block (summarize.py:44-52) may
+ * straddle ranks.  Every rank holding part of block b calls vb_block_piece on
+ * its frames of b, in recording order: frames [mean_off, mean_off + mean_n)
+ * of frames_dev are the block's own frames -- warped (vectors_dev), written to
+ * corrected_dev ([mean_n][h][w], NULL = not kept) and added, frame by frame,
+ * onto the float64 running sum partial_sum_dev[h][w] (zeros for the block's
+ * first piece; the same adds as spatial_summary, summarize.py:55-57, so the
+ * chained sum is bit-identical); all n_frames frames (own frames plus, with
+ * the high-pass, halo frames) are smoothed into smoothed_dev [n_frames][h][w].
+ * The running sum and the smoothed frames travel to the next contributor
+ * (NCCL send/recv); the rank holding the block's last frame calls
+ * vb_block_finish on the assembled buffer (recording frames [s_lo, s_lo +
+ * n_smoothed)): spatial = f32(sum / count), temporal = max - median
+ * (summarize.py:76-92; over x - mean_N(x) when highpass_window > 1). */
+int vb_block_piece(const void* frames_dev, int dtype, const vb_motion* vectors_dev, int64_t n_frames, int height,
+                   int width, const double* weights, int wradius, const float* gain_dev, int64_t mean_off,
+                   int64_t mean_n, float* corrected_dev, float* smoothed_dev, double* partial_sum_dev,
+                   void* stream);
+int vb_block_finish(const float* smoothed_dev, int64_t s_lo, int64_t n_smoothed, int64_t t0, int64_t count,
+                    int64_t t_total, int highpass_window, int height, int width, const double* sum_dev,
+                    float* spatial_dev, float* temporal_dev, void* stream);
+
 /* ---------------- whole stage, host buffers (drop-in boundary) ---------------- */
 typedef struct vb_stage_config {
     int height, width;

@@ -63,6 +63,8 @@ SIGNATURES = {
     "vb_extract_traces": (_i32, [_vp, _i64, _i32, _i32, _vp, _vp, _i32, _vp, _vp]),
     "vb_summarize_ex": (_i32, [_vp, _i32, _vp, _i64, _i32, _i32, _i32, _vp, _i32, C.POINTER(VbSummaryOpts),
                                _vp, _vp, _vp, _vp]),
+    "vb_block_piece": (_i32, [_vp, _i32, _vp, _i64, _i32, _i32, _vp, _i32, _vp, _i64, _i64, _vp, _vp, _vp, _vp]),
+    "vb_block_finish": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "vb_shading_gain": (_i32, [_vp, _i32, _i32, _vp, _i32, _vp, _vp]),
     "vb_correct_frames_ex": (_i32, [_vp, _i32, _i64, _i32, _i32, _vp, _vp, _vp, _vp]),
     "vb_stage_set_highpass": (_i32, [_vp, _i32]),

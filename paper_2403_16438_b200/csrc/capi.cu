@@ -408,6 +408,34 @@ int vb_summarize(const void* frames_dev, int dtype, const vb_motion* vectors_dev
                             wradius, corrected_dev, spatial_dev, temporal_dev, (cudaStream_t)stream);
 }
 
+int vb_block_piece(const void* frames_dev, int dtype, const vb_motion* vectors_dev, int64_t n_frames, int height,
+                   int width, const double* weights, int wradius, const float* gain_dev, int64_t mean_off,
+                   int64_t mean_n, float* corrected_dev, float* smoothed_dev, double* partial_sum_dev,
+                   void* stream) {
+    if (dtype != VB_U16 && dtype != VB_F32) return fail(VB_EINVAL, "unsupported sample type");
+    if (n_frames < 0 || mean_off < 0 || mean_n < 0 || mean_off + mean_n > n_frames)
+        return fail(VB_EINVAL, "block piece outside the frame buffer");
+    if (!weights || wradius < 0 || (n_frames > 0 && !smoothed_dev) || (mean_n > 0 && !partial_sum_dev))
+        return fail(VB_EINVAL, "null argument");
+    return launch_block_piece(frames_dev, dtype, vectors_dev, n_frames, height, width, weights, wradius, gain_dev,
+                              mean_off, mean_n, corrected_dev, smoothed_dev, partial_sum_dev, (cudaStream_t)stream);
+}
+
+int vb_block_finish(const float* smoothed_dev, int64_t s_lo, int64_t n_smoothed, int64_t t0, int64_t count,
+                    int64_t t_total, int highpass_window, int height, int width, const double* sum_dev,
+                    float* spatial_dev, float* temporal_dev, void* stream) {
+    if (count < 2) return fail(VB_EINVAL, "temporal summary needs at least 2 frames");  // summarize.py:79-80
+    if (!smoothed_dev || !sum_dev || !spatial_dev || !temporal_dev) return fail(VB_EINVAL, "null argument");
+    if (highpass_window > 1 && highpass_window % 2 == 0) return fail(VB_EINVAL, "high-pass window must be odd");
+    const int64_t hh = highpass_window > 1 ? highpass_window / 2 : 0;
+    const int64_t need_lo = hh ? std::max<int64_t>(0, t0 - hh) : t0;
+    const int64_t need_hi = hh ? std::min<int64_t>(t_total, t0 + count + hh) : t0 + count;
+    if (t0 < 0 || t0 + count > t_total || need_lo < s_lo || need_hi > s_lo + n_smoothed)
+        return fail(VB_EINVAL, "block frames not in the smoothed buffer");
+    return launch_block_finish(smoothed_dev, s_lo, t0, (int)count, t_total, highpass_window > 1 ? highpass_window : 0,
+                               (int64_t)height * width, sum_dev, spatial_dev, temporal_dev, (cudaStream_t)stream);
+}
+
 int vb_smooth_frames(const void* frames_dev, int dtype, int64_t n_frames, int height, int width,
                      const double* weights, int wradius, float* out_dev, void* stream) {
     if (dtype != VB_U16 && dtype != VB_F32) return fail(VB_EINVAL, "unsupported sample type");

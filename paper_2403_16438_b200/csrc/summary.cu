@@ -881,6 +881,96 @@ int launch_summarize_ex(const void* frames, int dtype, const vb_motion* vec, int
     return rc;
 }
 
+// ------------------------------------------------- blocks split across time shards
+// with frame-balanced shards a block may straddle ranks.  Each
+// contributing rank runs launch_block_piece on its frames of the block (in
+// recording order): the corrected frames continue the block's float64 running
+// sum -- the same sequence of adds block_mean_kernel performs, so the chained
+// sum is bit-identical -- and the smoothed frames are appended to the block's
+// smoothed buffer, which travels to the rank holding the block's last frame.
+// That rank runs launch_block_finish: mean = f32(sum / cnt) and the existing
+// max - median selection over the assembled buffer.
+
+// partial[i] += sum_t corrected[t][i], sequentially in frame order.
+__global__ void sum_continue_kernel(const float* __restrict__ frames, int64_t n, int64_t hw,
+                                    double* __restrict__ partial) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hw; i += (int64_t)gridDim.x * blockDim.x) {
+        const float* col = frames + i;
+        double s = partial[i];
+#pragma unroll 8
+        for (int64_t t = 0; t < n; ++t) s += (double)__ldcs(col + t * hw);
+        partial[i] = s;
+    }
+}
+
+__global__ void mean_finish_kernel(const double* __restrict__ sum, int64_t hw, int cnt, float* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hw; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (float)(sum[i] / (double)cnt);
+}
+
+int launch_block_piece(const void* frames, int dtype, const vb_motion* vec, int64_t n, int h, int w,
+                       const double* weights, int wradius, const float* gain, int64_t mean_off, int64_t mean_n,
+                       float* corrected, float* smoothed, double* partial, cudaStream_t s) {
+    if (n <= 0) return VB_OK;
+    if (wradius > kMaxWR) return fail(VB_EINVAL, "smoothing radius too large (max 16)");
+    const int64_t hw = (int64_t)h * w;
+    const size_t esz = dtype == VB_U16 ? 2 : 4;
+    auto at = [&](int64_t i) { return (const char*)frames + (size_t)i * hw * esz; };
+    auto vat = [&](int64_t i) { return vec ? vec + i : nullptr; };
+    float* corr = corrected;
+    float* scratch = nullptr;
+    keep_pool();
+    if (mean_n > 0 && !corr) {
+        VB_CUDA(cudaMallocAsync(&scratch, (size_t)mean_n * hw * sizeof(float), s));
+        corr = scratch;
+    }
+    const int64_t m1 = mean_off + mean_n;
+    int rc = launch_k3(at(0), dtype, vat(0), mean_off, h, w, weights, wradius, gain, nullptr, smoothed, s);
+    if (rc == VB_OK && mean_n > 0)
+        rc = launch_k3(at(mean_off), dtype, vat(mean_off), mean_n, h, w, weights, wradius, gain, corr,
+                       smoothed + (size_t)mean_off * hw, s);
+    if (rc == VB_OK)
+        rc = launch_k3(at(m1), dtype, vat(m1), n - m1, h, w, weights, wradius, gain, nullptr,
+                       smoothed + (size_t)m1 * hw, s);
+    if (rc == VB_OK && mean_n > 0) {
+        dim3 grid((unsigned)std::min<int64_t>((hw + 255) / 256, 1024));
+        {
+            ProfScope ps(kProfOther, s);
+            sum_continue_kernel<<<grid, 256, 0, s>>>(corr, mean_n, hw, partial);
+        }
+        launches().fetch_add(1, std::memory_order_relaxed);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) rc = cuda_fail(e, "sum_continue_kernel");
+    }
+    if (scratch) cudaFreeAsync(scratch, s);
+    return rc;
+}
+
+int launch_block_finish(const float* smoothed, int64_t s_lo, int64_t t0, int cnt, int64_t t_total, int hp_window,
+                        int64_t hw, const double* sum, float* spatial, float* temporal, cudaStream_t s) {
+    const int hh = hp_window > 1 ? hp_window / 2 : 0;
+    if (hh > kMaxHalfWindow) return fail(VB_EINVAL, "high-pass window too long (max 1025 frames)");
+    if (hh > 0 && cnt > 1024) return fail(VB_EINVAL, "temporal high-pass needs segment_length <= 1024");
+    {
+        dim3 grid((unsigned)std::min<int64_t>((hw + 255) / 256, 1024));
+        ProfScope ps(kProfOther, s);
+        mean_finish_kernel<<<grid, 256, 0, s>>>(sum, hw, cnt, spatial);
+    }
+    VB_LAUNCHED();
+    K4Args k4;
+    k4.sm = smoothed;
+    k4.s_lo = s_lo;
+    k4.g0 = t0;
+    k4.n = cnt;
+    k4.hw = hw;
+    k4.L = cnt;
+    k4.hh = hh;
+    k4.inv_n = 1.0 / (double)(2 * hh + 1);
+    k4.t_total = t_total;
+    k4.temporal = temporal;
+    return launch_median(k4, 1, s);
+}
+
 int launch_summarize(const void* frames, int dtype, const vb_motion* vec, int64_t n, int h, int w, int seg_len,
                      const double* weights, int wradius, float* corrected, float* spatial, float* temporal,
                      cudaStream_t s) {

@@ -101,6 +101,11 @@ struct SummaryOpts {
 int launch_summarize_ex(const void* frames, int dtype, const vb_motion* vec, int64_t n_avail, int h, int w,
                         int seg_len, const double* weights, int wradius, const SummaryOpts& o, float* corrected,
                         float* spatial, float* temporal, cudaStream_t s);
+int launch_block_piece(const void* frames, int dtype, const vb_motion* vec, int64_t n, int h, int w,
+                       const double* weights, int wradius, const float* gain, int64_t mean_off, int64_t mean_n,
+                       float* corrected, float* smoothed, double* partial, cudaStream_t s);
+int launch_block_finish(const float* smoothed, int64_t s_lo, int64_t t0, int cnt, int64_t t_total, int hp_window,
+                        int64_t hw, const double* sum, float* spatial, float* temporal, cudaStream_t s);
 int launch_shading_gain(const float* ref, int h, int w, const double* weights_host, int r, float* gain,
                         cudaStream_t s);
 int launch_smooth(const void* frames, int dtype, int64_t n, int h, int w, const double* weights, int wradius,

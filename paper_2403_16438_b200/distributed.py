@@ -137,3 +137,324 @@ class ShardedPreprocessor:
 
     def close(self):
         self.pre.close()
+
+
+# ------------------------------------------------------------------ frame-balanced shards
+# block-aligned shards cap strong scaling at ceil(K/N)/(K/N)
+# (C2 has K = 10 blocks; on 8 GPUs that is 62.5 %).  Frame-balanced shards give
+# every rank T/N frames of motion search and warp/smoothing; a block that
+# straddles a shard boundary is assembled at the rank holding its last frame:
+# earlier contributors send their smoothed frames (the block's samples for the
+# max - median selection, which does not decompose) and the block's float64
+# running sum (the spatial mean, continued add by add so it stays bit-identical
+# to one sequential pass) forward over NCCL point-to-point.  Whole blocks need
+# no exchange.  The high-pass halo (A17) is part of the smoothed range.
+
+
+def _range(n_frames: int, world: int, r: int) -> tuple[int, int]:
+    return n_frames * r // world, n_frames * (r + 1) // world
+
+
+def rank_of(n_frames: int, world: int, t: int) -> int:
+    """The rank whose balanced shard holds recording frame t."""
+    r = min(world - 1, (t * world) // max(n_frames, 1))
+    while r > 0 and _range(n_frames, world, r)[0] > t:
+        r -= 1
+    while _range(n_frames, world, r)[1] <= t:
+        r += 1
+    return r
+
+
+@dataclass(frozen=True)
+class Piece:
+    """This rank's share of a block that straddles a shard boundary."""
+    block: int
+    t0: int          # block frames [t0, t1)
+    t1: int
+    role: str        # "first" (sends), "middle" (receives, appends, sends), "last" (receives, owns)
+    prev: int | None  # contributor before / after this rank
+    next: int | None
+    s_lo: int        # recording frames of the owner's assembled smoothed buffer [s_lo, s_hi)
+    s_hi: int
+    c_lo: int        # frames this rank smooths into it [c_lo, c_hi)
+    c_hi: int
+    m_lo: int        # this rank's own frames of the block [m_lo, m_hi): corrected + running sum
+    m_hi: int
+
+
+@dataclass(frozen=True)
+class BalancedShard:
+    rank: int
+    world: int
+    frame_lo: int
+    frame_hi: int
+    n_total: int
+    segment_length: int
+    local_lo: int    # frames the rank holds: the shard plus the high-pass halo
+    local_hi: int
+    whole_lo: int    # recording frames of the blocks lying wholly inside the shard (block aligned)
+    whole_hi: int
+    head: Piece | None  # straddling block holding frame_lo (role middle or last)
+    tail: Piece | None  # straddling block holding frame_hi - 1 that this rank starts (role first)
+    block_lo: int    # blocks whose summaries this rank outputs (those whose last frame it holds)
+    block_hi: int
+
+    @property
+    def frames(self) -> int:
+        return self.frame_hi - self.frame_lo
+
+
+def balanced_plan(n_frames: int, segment_length: int, world: int, rank: int,
+                  highpass_window: int = 0) -> BalancedShard:
+    """Frame-balanced contiguous shard of rank `rank` and its straddling pieces."""
+    L = segment_length
+    if L < 2:
+        raise ValueError("segment length must be >= 2")
+    if n_frames % L == 1:  # summarize.py:79-80 on the final block
+        raise ValueError("temporal summary needs at least 2 frames")
+    hh = highpass_window // 2 if highpass_window and highpass_window > 1 else 0
+    T = n_frames
+    f0, f1 = _range(T, world, rank)
+    loc_lo, loc_hi = max(0, f0 - hh), min(T, f1 + hh)
+
+    def block(b):
+        return b * L, min(T, (b + 1) * L)
+
+    def piece(b):
+        t0, t1 = block(b)
+        starts, ends = t0 >= f0, t1 <= f1
+        role = "first" if starts else ("last" if ends else "middle")
+        prev = None if starts else rank_of(T, world, f0 - 1)
+        nxt = None if ends else rank_of(T, world, f1)
+        s_lo, s_hi = max(0, t0 - hh), min(T, t1 + hh)
+        c_lo = s_lo if starts else f0
+        c_hi = s_hi if ends else f1
+        return Piece(b, t0, t1, role, prev, nxt, s_lo, s_hi, c_lo, c_hi, max(t0, f0), min(t1, f1))
+
+    head = tail = None
+    whole_lo = whole_hi = f0
+    if f1 > f0:
+        b_first, b_last = f0 // L, (f1 - 1) // L
+        t0, t1 = block(b_first)
+        if t0 < f0 or (t1 > f1):
+            p = piece(b_first)
+            if p.role == "first":
+                tail = p
+            else:
+                head = p
+        t0l, t1l = block(b_last)
+        if b_last != b_first and t1l > f1:
+            tail = piece(b_last)
+        wb0 = b_first + (1 if (head is not None or tail is not None and tail.block == b_first) else 0)
+        wb1 = b_last + (0 if (tail is not None and tail.block == b_last) or (head is not None and head.block == b_last)
+                        else 1)
+        if wb1 > wb0:
+            whole_lo, whole_hi = block(wb0)[0], block(wb1 - 1)[1]
+    # owned blocks: those whose last frame lies in [f0, f1)
+    k = -(-T // L)
+    own = [b for b in range(k) if f0 <= block(b)[1] - 1 < f1]
+    b_lo, b_hi = (own[0], own[-1] + 1) if own else (0, 0)
+    return BalancedShard(rank, world, f0, f1, T, L, loc_lo, loc_hi, whole_lo, whole_hi, head, tail, b_lo, b_hi)
+
+
+class _P2P:
+    """Forward point-to-point transfers of straddling-block buffers.  NCCL
+    moves device tensors directly (one grouped launch per exchange); gloo (CPU
+    tests, single-GPU multi-rank checks) stages them through host memory."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.nccl = dist.get_backend(group) == "nccl"
+
+    def start(self, sends, recvs):
+        ops, post, keep = [], [], []
+        for tensors, peer in sends:
+            for t in tensors:
+                x = t if (self.nccl or not t.is_cuda) else t.cpu()
+                keep.append(x)
+                ops.append(dist.P2POp(dist.isend, x, peer, self.group))
+        for tensors, peer in recvs:
+            for t in tensors:
+                x = t if (self.nccl or not t.is_cuda) else torch.empty(t.shape, dtype=t.dtype)
+                post.append((t, x))
+                ops.append(dist.P2POp(dist.irecv, x, peer, self.group))
+        works = dist.batch_isend_irecv(ops) if ops else []
+        return works, post, keep
+
+    @staticmethod
+    def finish(handle):
+        works, post, _keep = handle
+        for w in works:
+            w.wait()
+        for t, x in post:
+            if x is not t:
+                t.copy_(x)
+
+
+class DeviceOps:
+    """The stage's CUDA entry points, as the balanced executor calls them."""
+
+    def __init__(self, pre):
+        self.pre = pre
+        self.cfg = pre.cfg
+
+    def template(self, frames, lo, hi, m, group):
+        from . import _device as D
+        from . import _lib
+
+        h, w = frames.shape[1:]
+        tsum = torch.zeros((h, w), dtype=torch.float64, device=frames.device)
+        if hi > lo:
+            _lib.call("vb_template_sum", frames[lo:hi].data_ptr(), D.vb_dtype(frames), hi - lo, h, w,
+                      tsum.data_ptr(), 0, D.stream_handle())
+        allreduce_sum_(tsum, group)
+        ref = torch.empty((h, w), dtype=torch.float32, device=frames.device)
+        _lib.call("vb_template_finish", tsum.data_ptr(), m, h * w, ref.data_ptr(), D.stream_handle())
+        self.pre.plan.set_reference(ref)
+        self.pre.set_shading(ref)
+
+    def estimate(self, frames):
+        from . import _device as D
+
+        vec = D.empty_motion(frames.shape[0], frames.device)
+        self.pre.plan.estimate(frames, self.cfg.subpixel, out=vec)
+        return vec
+
+    @staticmethod
+    def vec_slice(vec, a, b):
+        from . import _lib
+
+        rec = _lib.MOTION_DTYPE.itemsize
+        return vec[a * rec:b * rec]
+
+    def frames_buffer(self, n, like):
+        return torch.empty((n,) + tuple(like.shape[1:]), dtype=torch.float32, device=like.device)
+
+    def sum_buffer(self, like):
+        return torch.zeros(tuple(like.shape[1:]), dtype=torch.float64, device=like.device)
+
+    def whole(self, frames, vec, t_global0, t_total, interior, corrected_out):
+        from .summarize import summarize_device
+
+        c = self.cfg
+        return summarize_device(frames, c.segment_length, c.sigma, vectors_dev=vec, corrected_out=corrected_out,
+                                highpass_window=self.pre.window, gain=self.pre.gain, t_global0=t_global0,
+                                t_total=t_total, interior=interior)
+
+    def piece(self, frames, vec, mean_off, mean_n, corrected_out, smoothed, partial):
+        from . import _device as D
+        from . import _lib
+
+        n, h, w = frames.shape
+        pre = self.pre
+        _lib.call("vb_block_piece", frames.data_ptr(), D.vb_dtype(frames), D.ptr(vec), n, h, w,
+                  pre.weights.ctypes.data, pre.wradius, D.ptr(pre.gain), mean_off, mean_n, D.ptr(corrected_out),
+                  smoothed.data_ptr(), partial.data_ptr(), D.stream_handle())
+
+    def finish(self, smoothed, s_lo, t0, count, t_total, partial):
+        from . import _device as D
+        from . import _lib
+
+        n, h, w = smoothed.shape
+        sp = torch.empty((1, h, w), dtype=torch.float32, device=smoothed.device)
+        tp = torch.empty_like(sp)
+        _lib.call("vb_block_finish", smoothed.data_ptr(), s_lo, n, t0, count, t_total, self.pre.window, h, w,
+                  partial.data_ptr(), sp.data_ptr(), tp.data_ptr(), D.stream_handle())
+        return sp, tp
+
+
+@dataclass
+class ShardResult:
+    vectors: object          # vectors of every local frame (shard + halo)
+    spatial: torch.Tensor    # [block_hi - block_lo, H, W]: the blocks this rank owns
+    temporal: torch.Tensor
+    corrected: torch.Tensor | None  # the shard's own frames
+    n_frames: int
+
+    def vectors_numpy(self):
+        from . import _device as D
+
+        return D.motion_to_numpy(self.vectors, self.n_frames)
+
+
+class BalancedShardedPreprocessor:
+    """Per-rank driver over frame-balanced shards (balanced_plan):
+    template all-reduce -> motion search of every local frame -> the tail
+    piece is smoothed and sent forward while the whole blocks are summarised
+    -> the head piece is received, completed and (if this rank holds the
+    block's last frame) finished.  `ops` defaults to the CUDA entry points;
+    the CPU tests pass an oracle-backed stand-in to check the protocol."""
+
+    def __init__(self, height: int, width: int, config=None, group=None, ops=None):
+        if ops is None:
+            from . import stage
+
+            ops = DeviceOps(stage.DevicePreprocessor(height, width, config))
+        self.ops = ops
+        self.group = group
+        self.height, self.width = height, width
+
+    def run(self, frames_local, shard: BalancedShard, ref_frames: int, corrected_out=None) -> ShardResult:
+        """frames_local = recording frames [shard.local_lo, shard.local_hi);
+        corrected_out (optional) = [shard.frames, H, W] for the shard's own frames."""
+        ops, s = self.ops, shard
+        base, T, f0 = s.local_lo, s.n_total, s.frame_lo
+        if frames_local.shape[0] != s.local_hi - s.local_lo:
+            raise ValueError("frames_local must hold the shard and its halo")
+        lo, hi = template_rows(Shard(s.rank, s.world, s.frame_lo, s.frame_hi, 0, 0, T), ref_frames, base)
+        ops.template(frames_local, lo, hi, min(ref_frames, T), self.group)
+        vec = ops.estimate(frames_local)
+
+        def corr(a, b):
+            return None if corrected_out is None else corrected_out[a - f0:b - f0]
+
+        def run_piece(p: Piece, smoothed, acc):
+            ops.piece(frames_local[p.c_lo - base:p.c_hi - base], ops.vec_slice(vec, p.c_lo - base, p.c_hi - base),
+                      p.m_lo - p.c_lo, p.m_hi - p.m_lo, corr(p.m_lo, p.m_hi), smoothed, acc)
+
+        p2p = _P2P(self.group) if s.world > 1 else None
+        sends, recvs = [], []
+        if s.tail is not None:  # this rank starts a block that a later rank finishes
+            tb = ops.frames_buffer(s.tail.c_hi - s.tail.c_lo, frames_local)
+            ts = ops.sum_buffer(frames_local)
+            run_piece(s.tail, tb, ts)
+            sends.append(([tb, ts], s.tail.next))
+        head_buf = head_sum = None
+        if s.head is not None:
+            p = s.head
+            head_buf = ops.frames_buffer(p.c_hi - p.s_lo, frames_local)
+            head_sum = ops.sum_buffer(frames_local)
+            recvs.append(([head_buf[:p.c_lo - p.s_lo], head_sum], p.prev))
+        handle = p2p.start(sends, recvs) if (sends or recvs) else None
+        sp_parts, tp_parts = [], []
+        whole = None
+        if s.whole_hi > s.whole_lo:
+            whole = ops.whole(frames_local, vec, base, T, (s.whole_lo - base, s.whole_hi - s.whole_lo),
+                              corr(s.whole_lo, s.whole_hi))
+        if handle is not None:
+            p2p.finish(handle)
+        if s.head is not None:
+            p = s.head
+            # continue the received running sum with this rank's frames, append its smoothed frames
+            run_piece(p, head_buf[p.c_lo - p.s_lo:], head_sum)
+            if p.role == "middle":
+                p2p.finish(p2p.start([([head_buf, head_sum], p.next)], []))
+            else:
+                sp_h, tp_h = ops.finish(head_buf, p.s_lo, p.t0, p.t1 - p.t0, T, head_sum)
+                sp_parts.append(sp_h)
+                tp_parts.append(tp_h)
+        if whole is not None:
+            sp_parts.append(whole[0])
+            tp_parts.append(whole[1])
+        if sp_parts:
+            sp, tp = torch.cat(sp_parts), torch.cat(tp_parts)
+        else:
+            sp = torch.empty((0, self.height, self.width), dtype=torch.float32, device=frames_local.device)
+            tp = sp.clone()
+        assert sp.shape[0] == s.block_hi - s.block_lo
+        return ShardResult(vec, sp, tp, corrected_out, frames_local.shape[0])
+
+    def close(self):
+        close = getattr(getattr(self.ops, "pre", None), "close", None)
+        if close is not None:
+            close()
