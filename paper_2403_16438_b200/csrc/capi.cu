@@ -201,6 +201,47 @@ static int choose_group_size(const std::vector<int32_t>& o, int patch, int radiu
     return best_g;
 }
 
+// Row pitch of the search kernel's f32 region.  A warp's lanes are (patch,
+// dy) items reading region[dy * pitch + col_p + i] in lock step (the same i),
+// so the shared-memory wavefronts per LDS are fixed by the residues of
+// dy * pitch + col_p mod 32.  Pick the odd pitch in [max_wu, max_wu + 64)
+// with the fewest wavefronts over every warp of every group (ties: smallest).
+static int choose_pitch(const std::vector<PatchGroup>& groups, const std::vector<int32_t>& col, int S,
+                        int max_wu) {
+    int best_pitch = max_wu | 1;
+    long long best = -1;
+    for (int pitch = max_wu | 1; pitch < max_wu + 64; pitch += 2) {
+        long long cost = 0;
+        for (const auto& g : groups) {
+            const int items = g.count * S;
+            for (int w0 = 0; w0 < items; w0 += 32) {
+                int addr[32], n = 0;
+                for (int it = w0; it < std::min(items, w0 + 32); ++it) {
+                    const int p = it / S, dy = it % S;
+                    addr[n++] = dy * pitch + col[g.first + p];
+                }
+                int worst = 0;
+                for (int b = 0; b < 32; ++b) {
+                    int m = 0;
+                    for (int i = 0; i < n; ++i) {
+                        if (((addr[i] % 32) + 32) % 32 != b) continue;
+                        bool dup = false;
+                        for (int j = 0; j < i; ++j) dup |= addr[j] == addr[i];
+                        m += dup ? 0 : 1;
+                    }
+                    worst = std::max(worst, m);
+                }
+                cost += worst;
+            }
+        }
+        if (best < 0 || cost < best) {
+            best = cost;
+            best_pitch = pitch;
+        }
+    }
+    return best_pitch;
+}
+
 extern "C" {
 
 const char* vb_version(void) { return "voltb200 0.1 (sm_100a)"; }
@@ -259,6 +300,9 @@ int vb_motion_plan_create(vb_motion_plan** out, int height, int width, int patch
         t.max_g = std::max(t.max_g, (int)g.count);
         t.max_wu = std::max(t.max_wu, (int)g.wu);
     }
+    static const char* force_pitch = getenv("VB_PITCH");  // experiment knob (0 = max_wu | 1)
+    t.pitch = force_pitch ? atoi(force_pitch) : choose_pitch(groups, col, 2 * radius + 1, t.max_wu);
+    if (t.pitch < t.max_wu) t.pitch = t.max_wu | 1;
     cudaError_t e = cudaSuccess;
     e = e ? e : cudaMalloc(&t.tmpl, (size_t)n_origins * patch * t.tp * sizeof(float));
     e = e ? e : cudaMalloc(&t.rvar, 2 * (size_t)n_origins * sizeof(double));

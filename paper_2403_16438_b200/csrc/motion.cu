@@ -115,6 +115,7 @@ struct ZnccArgs {
     int w;
     int P, R, S, tp;
     int nch;        // dx chunks per (patch, dy) item (1 on the fast path)
+    int rows;       // dy rows per patch in the item space (S; < S only in timing experiments)
     int pitch_cap;  // f32 region pitch (odd, >= max wu)
     int bw, bh;     // raw box width / height in samples (bh = P + 2R)
     int bhc;        // TMA box height (the raw box is fetched as ceil(bh/bhc) row chunks)
@@ -334,15 +335,88 @@ __device__ __forceinline__ void cross_row(const float* __restrict__ reg, int pit
     }
 }
 
-// Search kernel: persistent over frames (blockIdx.y, +gridDim.y, ...).  Per
-// frame: wait for the TMA box, convert it to the centred f32 region, issue
-// the next frame's TMA into the now-free raw buffer, run the register-tiled
-// cross sums, then z = cov * inv summed over the group's patches in fixed
-// order.
-template <int P_CT, int S_CT>
-__global__ void __launch_bounds__(256) zncc_group_kernel(ZnccArgs a, const __grid_constant__ CUtensorMap tmap) {
+// S = 17 (search radius 8) with 16 lanes per patch: (G patches x 17 rows)
+// would leave 8 of every 136 lanes' worth of a fifth warp busy, so each patch
+// gets one half-warp.  Lane l owns candidate row d = l (< 8) or l + 1, and the
+// middle row M = 8 is shared: its 21 (frame row, template row) products are
+// spread over the lanes at two common iterations -- yy = 8, where lane d adds
+// frame row d + 8 with template row d (16 rows), and yy = 12, where lanes
+// d in {4, 13..16} add template rows {8, 17..20} -- so every window sample
+// loaded for the lane's own row serves the shared row too.  The half-warp
+// then sums the shared row's partials in a fixed shuffle tree.
+#ifndef VB_SPLIT_MIN_BLOCKS
+#define VB_SPLIT_MIN_BLOCKS 4  // measured: 113 regs x 4 CTAs beats a 96-reg cap with spills
+#endif
+constexpr int kSplitMinBlocks = VB_SPLIT_MIN_BLOCKS;
+
+template <int P>
+__device__ __forceinline__ void cross_row_split17(const float* __restrict__ reg, int pitch,
+                                                  const float* __restrict__ trow0, int tp, int d, float (&acc)[17],
+                                                  float (&accm)[17]) {
+    constexpr int S = 17, M = 8;
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+        acc[i] = 0.0f;
+        accm[i] = 0.0f;
+    }
+    const bool second = d == 4 || d >= 13;
+#pragma unroll 1
+    for (int yy = 0; yy < P; ++yy) {
+        const float* fr = reg + yy * pitch;
+        float win[S + P - 1];
+#pragma unroll
+        for (int i = 0; i < S + P - 1; ++i) win[i] = fr[i];
+        float tv[(P + 3) / 4 * 4];
+        {
+            const float4* trow = reinterpret_cast<const float4*>(trow0 + yy * tp);
+#pragma unroll
+            for (int q = 0; q < (P + 3) / 4; ++q) {
+                const float4 t4 = __ldg(trow + q);
+                tv[4 * q] = t4.x;
+                tv[4 * q + 1] = t4.y;
+                tv[4 * q + 2] = t4.z;
+                tv[4 * q + 3] = t4.w;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < S + P - 1; ++i) {
+#pragma unroll
+            for (int xx = (i - (S - 1) > 0 ? i - (S - 1) : 0); xx <= (i < P - 1 ? i : P - 1); ++xx)
+                acc[i - xx] = fmaf(win[i], tv[xx], acc[i - xx]);
+        }
+        if (yy == M || (yy == M + 4 && second)) {
+            const float4* trow = reinterpret_cast<const float4*>(trow0 + (d + yy - M) * tp);
+#pragma unroll
+            for (int q = 0; q < (P + 3) / 4; ++q) {
+                const float4 t4 = __ldg(trow + q);
+                tv[4 * q] = t4.x;
+                tv[4 * q + 1] = t4.y;
+                tv[4 * q + 2] = t4.z;
+                tv[4 * q + 3] = t4.w;
+            }
+#pragma unroll
+            for (int i = 0; i < S + P - 1; ++i) {
+#pragma unroll
+                for (int xx = (i - (S - 1) > 0 ? i - (S - 1) : 0); xx <= (i < P - 1 ? i : P - 1); ++xx)
+                    accm[i - xx] = fmaf(win[i], tv[xx], accm[i - xx]);
+            }
+        }
+    }
+}
+
+// Search kernel: persistent over frames (blockIdx.y, +gridDim.y, ...), FPI
+// frames per iteration.  Per iteration: wait for the TMA boxes, convert them to
+// centred f32 regions, issue the next iteration's TMA into the now-free raw
+// buffers, run the register-tiled cross sums, then z = cov * inv summed over
+// the group's patches in fixed order.  An item is one (frame, patch, dy) row
+// of S candidates; FPI = 2 packs G*S items of two frames into whole warps
+// (G = 8, S = 17: 272 items in 9 warps = 94 % of the lanes busy, against
+// 136 in 5 warps = 85 % with one frame).  The cov rows alias the region,
+// which is dead once every thread holds its accumulators.
+template <int P_CT, int S_CT, int FPI, bool SPLIT = false>
+__global__ void __launch_bounds__(SPLIT ? 128 : 288, SPLIT ? kSplitMinBlocks : 1) zncc_group_kernel(ZnccArgs a, const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bar;
+    __shared__ __align__(8) uint64_t bar[FPI];
     const int P = P_CT ? P_CT : a.P;
     const int S = S_CT ? S_CT : a.S;
     const int R = (S - 1) / 2;
@@ -352,87 +426,146 @@ __global__ void __launch_bounds__(256) zncc_group_kernel(ZnccArgs a, const __gri
     const int G = grp.count, wu = grp.wu;
     const int pitch = a.pitch_cap;
     const int SS = S * S;
-    float* s_reg = reinterpret_cast<float*>(smem + a.off_reg);  // [RH][pitch]
-    float* s_cov = reinterpret_cast<float*>(smem + a.off_z);    // [G][S*S]
-    float* s_tmpl = reinterpret_cast<float*>(smem + a.off_t);   // [G][P][tp] (fast path)
+    const size_t raw_slot = (size_t)a.off_reg / FPI;        // raw boxes at [0, off_reg)
+    const size_t reg_slot = (size_t)(a.off_z - a.off_reg) / FPI;  // regions (cov aliased) at [off_reg, off_z)
     const int tid = threadIdx.x, nth = blockDim.x;
-    constexpr bool kTmplSmem = false;  // measured: L1-resident taps beat an smem copy (occupancy)
-    if constexpr (kTmplSmem && P_CT != 0 && S_CT != 0) {
-        const float4* src = reinterpret_cast<const float4*>(a.tmpl + (size_t)grp.first * P * tp);
-        float4* dst = reinterpret_cast<float4*>(s_tmpl);
-        for (int i = tid; i < G * P * tp / 4; i += nth) dst[i] = __ldg(src + i);
-    }
     const float cg = group_centre(a, grp);
     const float magic = 8388608.0f + cg;
     const int boff = box_off(a, grp);
     if (tid == 0 && a.use_tma) {
-        mbar_init(&bar, 1);
+#pragma unroll
+        for (int f = 0; f < FPI; ++f) mbar_init(&bar[f], 1);
         fence_mbar_init();
         tma_prefetch_desc(&tmap);
     }
     __syncthreads();
     uint32_t phase = 0;
+    const int64_t gy = gridDim.y;
+    auto fetch = [&](int64_t t0) {
+#pragma unroll
+        for (int f = 0; f < FPI; ++f)
+            if (t0 + f * gy < a.n_frames) fetch_box(a, &tmap, grp, t0 + f * gy, smem + f * raw_slot, &bar[f]);
+    };
     int64_t t = blockIdx.y;
-    if (t < a.n_frames) fetch_box(a, &tmap, grp, t, smem, &bar);
-    for (; t < a.n_frames; t += gridDim.y) {
-        __syncthreads();  // plain-path box visible; region/cov of the previous frame consumed
-        box_ready(a, &bar, phase);
-        // raw box -> centred f32 region: warps over rows, lanes over columns
-        // (no per-element index division)
+    if (t < a.n_frames) fetch(t);
+    for (; t < a.n_frames; t += FPI * gy) {
+        int nf = 0;
+#pragma unroll
+        for (int f = 0; f < FPI; ++f) nf += (t + f * gy < a.n_frames) ? 1 : 0;
+        __syncthreads();  // plain-path boxes visible; previous partial phase done with the cov rows
+        if (a.use_tma) {
+            for (int f = 0; f < nf; ++f) mbar_wait(&bar[f], phase);
+            phase ^= 1u;
+        }
+        // raw boxes -> centred f32 regions: warps over rows, lanes over columns
         {
             const int lane = tid & 31, nw = nth >> 5;
-            if (a.dtype == VB_U16) {
-                const uint16_t* raw = reinterpret_cast<const uint16_t*>(smem) + boff;
-                for (int r = tid >> 5; r < RH; r += nw)
-                    for (int c = lane; c < wu; c += 32) s_reg[r * pitch + c] = u16_minus(raw[r * a.bw + c], magic);
-            } else {
-                const float* raw = reinterpret_cast<const float*>(smem) + boff;
-                for (int r = tid >> 5; r < RH; r += nw)
-                    for (int c = lane; c < wu; c += 32) s_reg[r * pitch + c] = __fsub_rn(raw[r * a.bw + c], cg);
+            for (int fr = tid >> 5; fr < nf * RH; fr += nw) {
+                const int f = fr / RH, r = fr - f * RH;
+                float* reg = reinterpret_cast<float*>(smem + a.off_reg + f * reg_slot) + r * pitch;
+                if (a.dtype == VB_U16) {
+                    const uint16_t* raw = reinterpret_cast<const uint16_t*>(smem + f * raw_slot) + boff + r * a.bw;
+                    for (int c = lane; c < wu; c += 32) reg[c] = u16_minus(raw[c], magic);
+                } else {
+                    const float* raw = reinterpret_cast<const float*>(smem + f * raw_slot) + boff + r * a.bw;
+                    for (int c = lane; c < wu; c += 32) reg[c] = __fsub_rn(raw[c], cg);
+                }
             }
         }
         __syncthreads();
-        if (t + gridDim.y < a.n_frames) fetch_box(a, &tmap, grp, t + gridDim.y, smem, &bar);  // raw box is free
-        const int nitems = G * S * a.nch;
-        for (int it = tid; it < nitems; it += nth) {
-            const int dy = it % S;
-            const int pc = it / S;
-            const int p = pc / a.nch, ch = pc - p * a.nch;
-            const int col = a.patch_col[grp.first + p];
-            const float* reg = s_reg + dy * pitch + col;
-            const float* trow0 = (kTmplSmem && P_CT != 0 && S_CT != 0) ? s_tmpl + (size_t)p * P * tp
-                                                                       : a.tmpl + (size_t)(grp.first + p) * P * tp;
-            float* z = s_cov + (size_t)p * SS + dy * S;
-            if constexpr (P_CT != 0 && S_CT != 0) {
-                float acc[S_CT];
-                cross_row<P_CT, S_CT>(reg, pitch, trow0, tp, acc);
-#pragma unroll
-                for (int d = 0; d < S_CT; ++d) z[d] = acc[d];
+        if (t + FPI * gy < a.n_frames) fetch(t + FPI * gy);  // raw boxes are free
+        const int per_frame = G * a.rows * a.nch;
+        const int nitems = nf * per_frame;
+        // fast path: one item per thread, cov rows alias the dead regions;
+        // generic path: items loop over the block, cov rows in their own slots
+        constexpr bool kOneRound = P_CT != 0 && S_CT != 0;
+        auto cov_at = [&](int f) -> float* {
+            return kOneRound ? reinterpret_cast<float*>(smem + a.off_reg + f * reg_slot)
+                             : reinterpret_cast<float*>(smem + a.off_z + f * (size_t)(a.off_t - a.off_z) / FPI);
+        };
+        if constexpr (SPLIT) {
+            // one (frame, patch, lane) item per thread, 16 lanes per patch
+            const int it = tid;
+            const bool valid = it < nitems;
+            const int f = valid ? it / per_frame : 0;
+            const int rem = it - f * per_frame;
+            const int p = rem >> 4, l = rem & 15;
+            const int d = l < 8 ? l : l + 1;
+            float acc[17], accm[17];
+            if (valid) {
+                const int col = a.patch_col[grp.first + p];
+                const float* reg = reinterpret_cast<const float*>(smem + a.off_reg + f * reg_slot) + d * pitch + col;
+                cross_row_split17<21>(reg, pitch, a.tmpl + (size_t)(grp.first + p) * P * tp, tp, d, acc, accm);
             } else {
-                float acc[kGenericDXB];
 #pragma unroll
-                for (int d = 0; d < kGenericDXB; ++d) acc[d] = 0.0f;
-                const int dx0 = ch * kGenericDXB;
-                for (int yy = 0; yy < P; ++yy) {
-                    const float* fr = reg + yy * pitch + dx0;
-                    const float* trow = trow0 + yy * tp;
-                    for (int xx = 0; xx < P; ++xx) {
-                        const float tv = __ldg(trow + xx);
+                for (int i = 0; i < 17; ++i) acc[i] = accm[i] = 0.0f;
+            }
 #pragma unroll
-                        for (int d = 0; d < kGenericDXB; ++d) acc[d] = fmaf(fr[xx + d], tv, acc[d]);
+            for (int i = 0; i < 17; ++i) {
+#pragma unroll
+                for (int off = 8; off >= 1; off >>= 1) accm[i] += __shfl_down_sync(0xffffffffu, accm[i], off, 16);
+            }
+            __syncthreads();  // every region read: the cov rows may overwrite them
+            if (valid) {
+                float* z = cov_at(f) + (size_t)p * SS;
+#pragma unroll
+                for (int i = 0; i < 17; ++i) z[d * 17 + i] = acc[i];
+                if (l == 0) {
+#pragma unroll
+                    for (int i = 0; i < 17; ++i) z[8 * 17 + i] = accm[i];
+                }
+            }
+        } else {
+        for (int it0 = 0; it0 < nitems; it0 += nth) {
+                const int it = it0 + tid;
+                float acc[S_CT ? S_CT : kGenericDXB];
+                int f = 0, p = 0, dy = 0, ch = 0;
+                if (it < nitems) {
+                    f = it / per_frame;
+                    const int rem = it - f * per_frame;
+                    dy = rem % a.rows;
+                    const int pc = rem / a.rows;
+                    p = pc / a.nch;
+                    ch = pc - p * a.nch;
+                    const int col = a.patch_col[grp.first + p];
+                    const float* reg = reinterpret_cast<const float*>(smem + a.off_reg + f * reg_slot) + dy * pitch + col;
+                    const float* trow0 = a.tmpl + (size_t)(grp.first + p) * P * tp;
+                    if constexpr (kOneRound) {
+                        cross_row<P_CT, S_CT>(reg, pitch, trow0, tp, acc);
+                    } else {
+#pragma unroll
+                        for (int d = 0; d < kGenericDXB; ++d) acc[d] = 0.0f;
+                        const int dx0 = ch * kGenericDXB;
+                        for (int yy = 0; yy < P; ++yy) {
+                            const float* fr = reg + yy * pitch + dx0;
+                            const float* trow = trow0 + yy * tp;
+                            for (int xx = 0; xx < P; ++xx) {
+                                const float tv = __ldg(trow + xx);
+#pragma unroll
+                                for (int d = 0; d < kGenericDXB; ++d) acc[d] = fmaf(fr[xx + d], tv, acc[d]);
+                            }
+                        }
                     }
                 }
+                if constexpr (kOneRound) __syncthreads();  // every region read: the cov rows may overwrite them
+                if (it < nitems) {
+                    float* z = cov_at(f) + (size_t)p * SS + dy * S;
+                    const int dx0 = kOneRound ? 0 : ch * kGenericDXB;
 #pragma unroll
-                for (int d = 0; d < kGenericDXB; ++d)
-                    if (dx0 + d < S) z[dx0 + d] = acc[d];
+                    for (int d = 0; d < (S_CT ? S_CT : kGenericDXB); ++d)
+                        if (kOneRound || dx0 + d < S) z[dx0 + d] = acc[d];
+                }
             }
         }
         __syncthreads();
-        double* part = a.partial + ((size_t)t * a.n_groups + blockIdx.x) * SS;
-        const float* inv = a.inv + ((size_t)t * a.n_patches + grp.first) * SS;
-        for (int c = tid; c < SS; c += nth) {
+        for (int c2 = tid; c2 < nf * SS; c2 += nth) {
+            const int ff = c2 / SS, c = c2 - ff * SS;
+            const int64_t tf = t + ff * gy;
+            const float* cov = cov_at(ff);
+            double* part = a.partial + ((size_t)tf * a.n_groups + blockIdx.x) * SS;
+            const float* inv = a.inv + ((size_t)tf * a.n_patches + grp.first) * SS;
             double s = 0.0;
-            for (int p = 0; p < G; ++p) s += (double)s_cov[(size_t)p * SS + c] * (double)__ldg(inv + (size_t)p * SS + c);
+            for (int q = 0; q < G; ++q) s += (double)cov[(size_t)q * SS + c] * (double)__ldg(inv + (size_t)q * SS + c);
             part[c] = s;
         }
     }
@@ -518,31 +651,31 @@ __global__ void finalize_kernel(const double* __restrict__ partial, int n_groups
 using KernelFn = void (*)(ZnccArgs, CUtensorMap);
 
 template <int S>
-static KernelFn fast_kernel_for() {
-    return zncc_group_kernel<21, S>;
+static KernelFn fast_kernel_for(int fpi) {
+    return fpi == 2 ? zncc_group_kernel<21, S, 2> : zncc_group_kernel<21, S, 1>;
 }
 
-static KernelFn pick_kernel(int P, int S, bool* fast) {
+static KernelFn pick_kernel(int P, int S, int fpi, bool* fast) {
     *fast = true;
     if (P == 21) {
         switch (S) {
-            case 3: return fast_kernel_for<3>();
-            case 5: return fast_kernel_for<5>();
-            case 7: return fast_kernel_for<7>();
-            case 9: return fast_kernel_for<9>();
-            case 11: return fast_kernel_for<11>();
-            case 13: return fast_kernel_for<13>();
-            case 15: return fast_kernel_for<15>();
-            case 17: return fast_kernel_for<17>();
-            case 19: return fast_kernel_for<19>();
-            case 21: return fast_kernel_for<21>();
-            case 23: return fast_kernel_for<23>();
-            case 25: return fast_kernel_for<25>();
+            case 3: return fast_kernel_for<3>(fpi);
+            case 5: return fast_kernel_for<5>(fpi);
+            case 7: return fast_kernel_for<7>(fpi);
+            case 9: return fast_kernel_for<9>(fpi);
+            case 11: return fast_kernel_for<11>(fpi);
+            case 13: return fast_kernel_for<13>(fpi);
+            case 15: return fast_kernel_for<15>(fpi);
+            case 17: return fast_kernel_for<17>(fpi);
+            case 19: return fast_kernel_for<19>(fpi);
+            case 21: return fast_kernel_for<21>(fpi);
+            case 23: return fast_kernel_for<23>(fpi);
+            case 25: return fast_kernel_for<25>(fpi);
             default: break;
         }
     }
     *fast = false;
-    return zncc_group_kernel<0, 0>;
+    return fpi == 2 ? zncc_group_kernel<0, 0, 2> : zncc_group_kernel<0, 0, 1>;
 }
 
 struct SmemPlan {
@@ -554,7 +687,8 @@ struct SmemPlan {
     size_t stats_off, stats_total;  // statistics kernel: raw box + [S][pitch] T2 + [S][pitch] T1
 };
 
-static SmemPlan zncc_smem(int P, int R, int max_g, int max_wu, int dtype) {
+static SmemPlan zncc_smem(int P, int R, int max_g, int max_wu, int dtype, int fpi = 1, bool alias = true,
+                          int pitch = 0) {
     const int S = 2 * R + 1, SS = S * S, RH = P + 2 * R;
     const size_t esz = dtype == VB_U16 ? 2 : 4;
     SmemPlan sp;
@@ -562,14 +696,19 @@ static SmemPlan zncc_smem(int P, int R, int max_g, int max_wu, int dtype) {
     // TMA box rows are 16-byte multiples and start 16-byte aligned (up to
     // 16/esz - 1 extra leading columns)
     sp.bw = (int)((((max_wu + 16 / esz - 1) * esz + 15) / 16) * 16 / esz);
-    sp.pitch = max_wu | 1;
+    sp.pitch = pitch > 0 ? pitch : (max_wu | 1);
     sp.bhc = std::min(sp.bh, 256);  // TMA box height limit (one chunk for P + 2R <= 256)
     const int rows = (sp.bh + sp.bhc - 1) / sp.bhc * sp.bhc;
     sp.raw_bytes = (((size_t)sp.bw * rows * esz) + 127) & ~(size_t)127;
-    sp.off_reg = sp.raw_bytes;
-    sp.off_z = (sp.off_reg + (size_t)RH * sp.pitch * 4 + 15) & ~(size_t)15;
-    sp.off_t = (sp.off_z + (size_t)max_g * SS * 4 + 15) & ~(size_t)15;
-    sp.total = sp.off_t;  // + max_g * P * tp * 4 with kTmplSmem
+    // search kernel: fpi raw boxes, fpi f32 regions (the cov rows alias a
+    // region on the fast path, else fpi separate cov slots)
+    const size_t region = (size_t)RH * sp.pitch * 4, cov = (size_t)max_g * SS * 4;
+    const size_t reg_slot = ((alias ? std::max(region, cov) : region) + 15) & ~(size_t)15;
+    const size_t cov_slot = alias ? 0 : (cov + 15) & ~(size_t)15;
+    sp.off_reg = fpi * sp.raw_bytes;
+    sp.off_z = sp.off_reg + fpi * reg_slot;
+    sp.off_t = sp.off_z + fpi * cov_slot;
+    sp.total = sp.off_t;
     sp.stats_off = sp.raw_bytes;
     sp.stats_total = sp.stats_off + (size_t)S * sp.pitch * (dtype == VB_U16 ? 8 + 4 : 8 + 8);
     return sp;
@@ -589,11 +728,30 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     if (n_frames <= 0) return VB_OK;
     const int S = 2 * radius + 1, SS = S * S;
     bool fast = false;
-    KernelFn fn = pick_kernel(patch, S, &fast);
+    pick_kernel(patch, S, 1, &fast);
+    // frames per search iteration: two when that packs the (frame, patch, dy)
+    // items into whole warps noticeably better and both frames fit
+    const int nch = fast ? 1 : (S + kGenericDXB - 1) / kGenericDXB;
+    const int items1 = t.max_g * S * nch;
+    int fpi = 1;
+    if (fast && 2 * items1 <= 288) {
+        const double e1 = (double)items1 / (((items1 + 31) / 32) * 32);
+        const double e2 = (double)(2 * items1) / (((2 * items1 + 31) / 32) * 32);
+        // measured on C2 (G = 8, S = 17): 94 % vs 85 % lanes did not pay for
+        // half the resident CTAs, so two frames only for a large lane gain
+        if (e2 > e1 + 0.15 && zncc_smem(patch, radius, t.max_g, t.max_wu, dtype, 2, true, t.pitch).total <= 112 * 1024)
+            fpi = 2;
+    }
+    static const char* force_fpi = getenv("VB_FPI");  // experiment knob
+    if (fast && force_fpi && (atoi(force_fpi) == 1 || atoi(force_fpi) == 2)) fpi = atoi(force_fpi);
+    // S = 17: half-warp per patch with the shared middle row (cross_row_split17)
+    static const char* no_split = getenv("VB_NO_SPLIT");  // experiment knob
+    const bool split = fast && patch == 21 && S == 17 && fpi == 1 && !no_split;
+    KernelFn fn = split ? zncc_group_kernel<21, 17, 1, true> : pick_kernel(patch, S, fpi, &fast);
     void (*stats_fn)(ZnccArgs, CUtensorMap) =
         patch == 21 ? (dtype == VB_U16 ? zncc_stats_kernel<true, 21> : zncc_stats_kernel<false, 21>)
                     : (dtype == VB_U16 ? zncc_stats_kernel<true, 0> : zncc_stats_kernel<false, 0>);
-    SmemPlan sp = zncc_smem(patch, radius, t.max_g, t.max_wu, dtype);
+    SmemPlan sp = zncc_smem(patch, radius, t.max_g, t.max_wu, dtype, fpi, fast, t.pitch);
     if (std::max(sp.total, sp.stats_total) > 227 * 1024)
         return fail(VB_EINVAL, "patch group does not fit in shared memory");
     VB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.total));
@@ -625,9 +783,11 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     static const bool no_tma = getenv("VB_NO_TMA") != nullptr;  // debug toggle: plain-load staging
     a.use_tma = !no_tma && make_frames_tmap(&tmap, frames, dtype, n_frames, h, w, sp.bhc, sp.bw) ? 1 : 0;
 
-    const int items = t.max_g * S * a.nch;
+    static const char* hack_rows = getenv("VB_HACK_ROWS");  // timing experiment only: WRONG results
+    a.rows = split ? 16 : (hack_rows ? std::min(S, atoi(hack_rows)) : S);
+    const int items = fpi * t.max_g * a.rows * nch;
     int threads = ((items + 31) / 32) * 32;
-    threads = std::max(64, std::min(threads, 256));
+    threads = std::max(64, std::min(threads, fast ? 288 : 256));
 
     // frame batches bound the float64 partials + f32 inv buffers to ~1 GB
     const size_t per_frame_part = (size_t)t.n_groups * SS * sizeof(double);

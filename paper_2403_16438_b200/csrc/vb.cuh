@@ -69,6 +69,7 @@ struct Templates {
     int32_t* patch_col = nullptr;// [N] column of the patch's dx=-R window inside its group union
     PatchGroup* groups = nullptr;// [n_groups]
     int n = 0, n_groups = 0, tp = 0, max_g = 0, max_wu = 0;
+    int pitch = 0;               // f32 region row pitch of the search kernel (bank-conflict tuned)
 };
 
 // Kernel entry points implemented in the .cu files (host-side launchers).
