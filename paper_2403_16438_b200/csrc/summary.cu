@@ -469,6 +469,210 @@ __global__ void __launch_bounds__(kK3Threads, 3) warp_smooth_tma_kernel(K3Args a
     }
 }
 
+// K3 v2: same tile, TMA box and float64 operation order as
+// warp_smooth_tma_kernel, restructured for fewer issued instructions (the
+// kernel is issue-bound, not FP64-pipe-bound):
+//  A1 the bilinear warp is separable -- translate's top/bottom rows are
+//     omx*a + fx*b of source rows ra and rc, and row y+1's bottom row is row
+//     y's top row -- so each raw-box row is interpolated horizontally once
+//     (f32, unfused, numpy's order) into sH, aliased onto sV;
+//  A2 corrected = omy*sH[ra] + fy*sH[rc] (+ shading), written once as f32
+//     output and once as f64 into sC;
+//  B  vertical pass: one thread per (column, third of the tile's rows), up to
+//     11 outputs from 29 loaded samples (2.6 loads/output instead of 5.5);
+//  C  horizontal pass: 8 outputs per thread from 26 samples, float4 stores.
+// The next frame's box is issued right after A1 (raw box consumed).
+constexpr int kVR2 = 11;  // vertical-pass outputs per thread: kTY = 11 + 11 + 10
+#ifndef VB_K3V2_MIN_BLOCKS
+#define VB_K3V2_MIN_BLOCKS 3  // measured: 80 regs x 3 CTAs beats a 64-reg cap (spills) x 4
+#endif
+constexpr int kK3V2MinBlocks = VB_K3V2_MIN_BLOCKS;
+template <int WR, bool U16>
+static size_t k3_v2_smem_bytes() {  // raw box | sC f32 [EH][EWP] | sV f32 [kTY][EWP] aliased by sH f32 [EH+1][EW]
+    constexpr int EH = kTY + 2 * WR, EW = kTX + 2 * WR, EWP = EW | 1;
+    constexpr int ALN = U16 ? 8 : 4;
+    constexpr int BWB = ((EW + 1 + ALN - 1 + ALN - 1) / ALN) * ALN;
+    const size_t raw = (((size_t)(EH + 1) * BWB * (U16 ? 2 : 4)) + 127) & ~(size_t)127;
+    return raw + (size_t)EH * EWP * sizeof(float) + std::max((size_t)kTY * EWP, (size_t)(EH + 1) * EW) * sizeof(float);
+}
+
+template <int WR, bool U16, bool SHADE>
+__global__ void __launch_bounds__(kK3Threads, kK3V2MinBlocks) warp_smooth_v2_kernel(K3Args a, const __grid_constant__ CUtensorMap tmap) {
+    constexpr int EH = kTY + 2 * WR, EW = kTX + 2 * WR, EWP = EW | 1;
+    constexpr int ALN = U16 ? 8 : 4;
+    constexpr int BWB = ((EW + 1 + ALN - 1 + ALN - 1) / ALN) * ALN;
+    constexpr int BHB = EH + 1;
+    constexpr int NCS = (EW + 31) / 32;
+
+    using S_T = typename std::conditional<U16, uint16_t, float>::type;
+    extern __shared__ __align__(128) unsigned char smem[];
+    S_T* sRaw = reinterpret_cast<S_T*>(smem);
+    // every intermediate is an f32 value (corrected samples; the vertical pass
+    // is rounded to f32 like scipy's per-pass output), so shared memory holds
+    // f32 and the passes widen to f64 on load: 43 KB per CTA instead of 64
+    float* sC = reinterpret_cast<float*>(smem + (((size_t)BHB * BWB * sizeof(S_T) + 127) & ~(size_t)127));  // [EH][EWP]
+    float* sV = sC + (size_t)EH * EWP;  // [kTY][EWP] vertical pass
+    float* sH = sV;                     // [BHB][EW] horizontal interpolations (phase A only; aliases sV)
+    __shared__ double s_w[WR + 1];
+    __shared__ int s_ra[EH], s_rc[EH], s_xa[EW], s_xb[EW];
+    __shared__ int s_gy[SHADE ? EH : 1], s_gx[SHADE ? EW : 1];
+    __shared__ int s_box[2];
+    __shared__ __align__(8) uint64_t bar;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid <= WR) s_w[tid] = a.wt.w[WR - tid];  // s_w[k] = weight at offset -k (symmetric)
+    const int ty0 = blockIdx.y * kTY, tx0 = blockIdx.x * kTX;
+    const int64_t hw = (int64_t)a.h * a.w;
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+        tma_prefetch_desc(&tmap);
+    }
+    __syncthreads();
+    auto issue = [&](int64_t t) {
+        const WarpOp op = make_warp(a.vec, t);
+        int y0, y1, x0, x1;
+        src_span(ty0 - WR, ty0 + kTY + WR, a.h, op.iy, y0, y1);
+        src_span(tx0 - WR, tx0 + kTX + WR, a.w, op.ix, x0, x1);
+        const int x0a = x0 & ~(ALN - 1);
+        mbar_expect_tx(&bar, (uint32_t)(BWB * BHB * sizeof(S_T)));
+        tma_load_3d(sRaw, &tmap, x0a, y0, (int)t, &bar);
+        return make_int2(x0a, y0);
+    };
+    auto smp = [](S_T v) -> float {
+        if constexpr (U16)
+            return u16_minus(v, 8388608.0f);
+        else
+            return v;
+    };
+    int2 origin_next = make_int2(0, 0);
+    int64_t t = blockIdx.z;
+    if (tid == 0 && t < a.n) origin_next = issue(t);
+    uint32_t phase = 0;
+    const double* wk = s_w;
+    for (; t < a.n; t += gridDim.z) {
+        const WarpOp op = make_warp(a.vec, t);
+        if (tid == 0) {
+            s_box[0] = origin_next.x;
+            s_box[1] = origin_next.y;
+        }
+        for (int i = tid; i < EH + EW; i += kK3Threads) {
+            if (i < EH) {
+                const int y = reflect_index(ty0 - WR + i, a.h);
+                if constexpr (SHADE) s_gy[i] = y;
+                s_ra[i] = clampi(y - op.iy, 0, a.h - 1);
+                s_rc[i] = clampi(y - op.iy - 1, 0, a.h - 1);
+            } else {
+                const int e = i - EH;
+                const int x = reflect_index(tx0 - WR + e, a.w);
+                if constexpr (SHADE) s_gx[e] = x;
+                s_xa[e] = clampi(x - op.ix, 0, a.w - 1);
+                s_xb[e] = clampi(x - op.ix - 1, 0, a.w - 1);
+            }
+        }
+        __syncthreads();  // tables + origin published; previous frame's passes done with sV/sC
+        const int bx0 = s_box[0], by0 = s_box[1];
+        int xa[NCS], xb[NCS];
+#pragma unroll
+        for (int k = 0; k < NCS; ++k) {
+            const int c = lane + 32 * k;
+            xa[k] = c < EW ? s_xa[c] - bx0 : 0;
+            xb[k] = c < EW ? s_xb[c] - bx0 : 0;
+        }
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+        // A1: horizontal interpolation of every box row
+        for (int r = warp; r < BHB; r += kK3Threads / 32) {
+            const S_T* row = sRaw + r * BWB;
+            float* hrow = sH + r * EW;
+#pragma unroll
+            for (int k = 0; k < NCS; ++k) {
+                const int c = lane + 32 * k;
+                if (c < EW) hrow[c] = __fadd_rn(__fmul_rn(op.omx, smp(row[xa[k]])), __fmul_rn(op.fx, smp(row[xb[k]])));
+            }
+        }
+        __syncthreads();
+        if (tid == 0 && t + gridDim.z < a.n) origin_next = issue(t + gridDim.z);  // raw box consumed
+        // A2: vertical interpolation -> corrected (f32 out, f64 into sC)
+        {
+            float* corr_base = a.corrected ? a.corrected + t * hw : nullptr;
+            int gxs[NCS];
+            if constexpr (SHADE) {
+#pragma unroll
+                for (int k = 0; k < NCS; ++k) gxs[k] = lane + 32 * k < EW ? s_gx[lane + 32 * k] : 0;
+            }
+            for (int ey = warp; ey < EH; ey += kK3Threads / 32) {
+                const float* ha = sH + (s_ra[ey] - by0) * EW;
+                const float* hc = sH + (s_rc[ey] - by0) * EW;
+                const int gy = ty0 + ey - WR;
+                const bool row_out = corr_base && ey >= WR && ey < WR + kTY && gy < a.h;
+                const float* grow = SHADE ? a.gain + (int64_t)s_gy[ey] * a.w : nullptr;
+#pragma unroll
+                for (int k = 0; k < NCS; ++k) {
+                    const int c = lane + 32 * k;
+                    if (c < EW) {
+                        float v = __fadd_rn(__fmul_rn(op.omy, ha[c]), __fmul_rn(op.fy, hc[c]));
+                        if constexpr (SHADE) v = __fdiv_rn(v, __ldg(grow + gxs[k]));
+                        sC[ey * EWP + c] = v;
+                        const int gx = tx0 + c - WR;
+                        if (row_out && c >= WR && c < WR + kTX && gx < a.w) corr_base[(int64_t)gy * a.w + gx] = v;
+                    }
+                }
+            }
+        }
+        __syncthreads();  // sC complete; sH (sV) free
+        // B: vertical 19-tap pass, (column, third of the rows) per thread
+        if (tid < 3 * EW) {
+            const int c = tid % EW, seg = tid / EW;
+            const int r0 = seg * kVR2;
+            const int nout = seg < 2 ? kVR2 : kTY - 2 * kVR2;
+            double x[kVR2 + 2 * WR];
+#pragma unroll
+            for (int q = 0; q < kVR2 + 2 * WR; ++q) x[q] = (r0 + q < EH) ? (double)sC[(r0 + q) * EWP + c] : 0.0;
+#pragma unroll
+            for (int j = 0; j < kVR2; ++j) {
+                if (j < nout) {
+                    double acc = __dmul_rn(x[j + WR], wk[0]);
+#pragma unroll
+                    for (int k = WR; k >= 1; --k)
+                        acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(x[j + WR - k], x[j + WR + k]), wk[k]));
+                    sV[(r0 + j) * EWP + c] = (float)acc;
+                }
+            }
+        }
+        __syncthreads();
+        // C: horizontal pass -> smoothed frame.  Lanes take consecutive rows.
+        {
+            constexpr int HR = 8;
+            const int ly = tid % kTY, lx0 = (tid / kTY) * HR;
+            double x[HR + 2 * WR];
+#pragma unroll
+            for (int q = 0; q < HR + 2 * WR; ++q) x[q] = (double)sV[ly * EWP + lx0 + q];
+            float o[HR];
+#pragma unroll
+            for (int j = 0; j < HR; ++j) {
+                double acc = __dmul_rn(x[j + WR], wk[0]);
+#pragma unroll
+                for (int k = WR; k >= 1; --k) acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(x[j + WR - k], x[j + WR + k]), wk[k]));
+                o[j] = (float)acc;
+            }
+            const int gy = ty0 + ly, gx0 = tx0 + lx0;
+            float* dst = a.smoothed + t * hw + (int64_t)gy * a.w + gx0;
+            if (gy < a.h) {
+                if ((a.w & 3) == 0 && gx0 + HR <= a.w) {
+#pragma unroll
+                    for (int j = 0; j < HR; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < HR; ++j)
+                        if (gx0 + j < a.w) dst[j] = o[j];
+                }
+            }
+        }
+    }
+}
+static_assert(kK3Threads == kTY * (kTX / 8), "horizontal pass maps one thread per (row, 8 outputs)");
+static_assert(3 * (kTX + 18) <= kK3Threads, "vertical pass maps one thread per (column, third)");
+
 template <int WR, bool U16>
 static size_t k3_tma_smem_bytes() {
     constexpr int EH = kTY + 2 * WR, EW = kTX + 2 * WR, EWP = EW | 1;
@@ -481,8 +685,10 @@ static size_t k3_tma_smem_bytes() {
 
 template <int WR, bool U16>
 static int launch_k3_tma(const CUtensorMap& tmap, K3Args a, int64_t n, int h, int w, cudaStream_t s) {
-    const size_t smem = k3_tma_smem_bytes<WR, U16>();
-    auto kern = a.gain ? warp_smooth_tma_kernel<WR, U16, true> : warp_smooth_tma_kernel<WR, U16, false>;
+    static const bool v1 = getenv("VB_K3_V1") != nullptr;  // experiment knob: the previous kernel
+    const size_t smem = v1 ? k3_tma_smem_bytes<WR, U16>() : k3_v2_smem_bytes<WR, U16>();
+    auto kern = v1 ? (a.gain ? warp_smooth_tma_kernel<WR, U16, true> : warp_smooth_tma_kernel<WR, U16, false>)
+                   : (a.gain ? warp_smooth_v2_kernel<WR, U16, true> : warp_smooth_v2_kernel<WR, U16, false>);
     VB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

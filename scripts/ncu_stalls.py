@@ -35,3 +35,27 @@ def main(path, regex, top=25):
 
 if __name__ == "__main__":
     main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 25)
+
+
+def opmix(path, regex):
+    """Executed warp instructions per opcode (source page)."""
+    out = subprocess.run(["ncu", "-i", path, "-k", f"regex:{regex}", "--page", "source", "--csv",
+                          "--print-source", "sass"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hdr = rows[1]
+    data = [r for r in rows[2:] if len(r) == len(hdr) and r[0].startswith("0x")]
+    seen, ops = set(), {}
+    for r in data:
+        if r[0] in seen:
+            continue
+        seen.add(r[0])
+        src = r[hdr.index("Source")].split()
+        if not src:
+            continue
+        op = src[1] if src[0].startswith("@") else src[0]
+        n = float(r[hdr.index("Instructions Executed")] or 0)
+        ops[op] = ops.get(op, 0) + n
+    tot = sum(ops.values())
+    print(f"{tot:.4g} warp instructions")
+    for k, v in sorted(ops.items(), key=lambda x: -x[1])[:40]:
+        print(f"  {k:28s} {v:12.4g} {v / tot:6.1%}")
