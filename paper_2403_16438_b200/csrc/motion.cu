@@ -135,7 +135,6 @@ struct ZnccArgs {
 };
 
 constexpr int kGenericDXB = 8;
-constexpr int kStatsDC = 6;  // dy rows per vertical sliding chain in the statistics kernel
 
 // Frame samples are centred on an integer c close to the group's template
 // level, so the f32 cross sums accumulate O(100) instead of O(1000)
@@ -196,9 +195,10 @@ __device__ __forceinline__ void box_ready(const ZnccArgs& a, uint64_t* bar, uint
 // 0 where the reference skips a dead patch or a flat window).  Camera (u16)
 // samples use exact integer arithmetic (int32 sums, int64 sums of squares,
 // n*fvar = n*S2 - S1^2 exactly) straight from the TMA-staged raw box; float32
-// input uses float64 sums.  Vertical chains run per (column, 4-row chunk) so
-// every thread has work.  The next frame's box is fetched while this frame's
-// horizontal pass runs.
+// input uses float64 sums.  One thread per union column slides its vertical
+// sums down all S rows (a single round for groups up to 256 columns wide),
+// then one thread per (patch, dy) row slides horizontally.  The next frame's
+// box is fetched while this frame's horizontal pass runs.
 template <bool INT, int P_CT>
 __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __grid_constant__ CUtensorMap tmap) {
     using T1 = typename std::conditional<INT, int, double>::type;        // sample / sum of f
@@ -214,7 +214,6 @@ __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __gri
     T1* v1 = reinterpret_cast<T1*>(smem + a.off_z + (size_t)S * a.pitch_cap * sizeof(T2));  // [S][vp]
     const float cg = group_centre(a, grp);
     const int cgi = (int)cg;
-    const int nchunk = (S + kStatsDC - 1) / kStatsDC;
     const int boff = box_off(a, grp);
     if (threadIdx.x == 0 && a.use_tma) {
         mbar_init(&bar, 1);
@@ -228,9 +227,8 @@ __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __gri
     for (; t < a.n_frames; t += gridDim.y) {
         __syncthreads();  // box visible (plain path) / V free (previous horizontal pass done)
         box_ready(a, &bar, phase);
-        for (int it = threadIdx.x; it < wu * nchunk; it += blockDim.x) {
-            const int c = it % wu, k = it / wu;
-            const int d0 = k * kStatsDC, nd = min(kStatsDC, S - d0);
+        // vertical window sums: one thread per union column, sliding down all S rows
+        for (int c = threadIdx.x; c < wu; c += blockDim.x) {
             auto sample = [&](int r) -> T1 {
                 if constexpr (INT)
                     return (int)reinterpret_cast<const uint16_t*>(smem)[r * a.bw + c + boff] - cgi;
@@ -242,18 +240,18 @@ __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __gri
 #pragma unroll
             for (int yy = 0; yy < (P_CT ? P_CT : 64); ++yy) {
                 if (!P_CT && yy >= P) break;
-                const T1 f = sample(d0 + yy);
+                const T1 f = sample(yy);
                 s1 += f;
                 s2 += (T2)f * (T2)f;
             }
-            v1[d0 * vp + c] = s1;
-            v2[d0 * vp + c] = s2;
-            for (int j = 1; j < nd; ++j) {
-                const T1 fo = sample(d0 + j - 1), fi = sample(d0 + j - 1 + P);
+            v1[c] = s1;
+            v2[c] = s2;
+            for (int dy = 1; dy < S; ++dy) {
+                const T1 fo = sample(dy - 1), fi = sample(dy - 1 + P);
                 s1 += fi - fo;
                 s2 += (T2)fi * (T2)fi - (T2)fo * (T2)fo;
-                v1[(d0 + j) * vp + c] = s1;
-                v2[(d0 + j) * vp + c] = s2;
+                v1[dy * vp + c] = s1;
+                v2[dy * vp + c] = s2;
             }
         }
         __syncthreads();
@@ -786,6 +784,9 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     static const char* hack_rows = getenv("VB_HACK_ROWS");  // timing experiment only: WRONG results
     a.rows = split ? 16 : (hack_rows ? std::min(S, atoi(hack_rows)) : S);
     const int items = fpi * t.max_g * a.rows * nch;
+    // statistics kernel: one thread per union column (vertical chains), then
+    // one per (patch, dy) row (horizontal chains)
+    const int stats_threads = std::max(64, std::min(256, (std::max(t.max_wu, t.max_g * S) + 31) / 32 * 32));
     int threads = ((items + 31) / 32) * 32;
     threads = std::max(64, std::min(threads, fast ? 288 : 256));
 
@@ -823,7 +824,7 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
             as.off_reg = 0;
             as.off_z = (int)sp.stats_off;
             ProfScope ps(kProfOther, s);
-            stats_fn<<<grid, 256, sp.stats_total, s>>>(as, tmap);
+            stats_fn<<<grid, stats_threads, sp.stats_total, s>>>(as, tmap);
         }
         launches().fetch_add(1, std::memory_order_relaxed);
         cudaError_t e = cudaGetLastError();
