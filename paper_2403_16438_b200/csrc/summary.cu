@@ -779,15 +779,103 @@ __device__ __forceinline__ uint32_t warp_select(const uint32_t (&v)[VPL], uint32
     return lo + ans;
 }
 
+// k-th smallest of the warp's keys in three steps instead of up to 32
+// bisection rounds over all VPL keys per lane: a 128-bin histogram of the top
+// 7 bits of key - lo (shared-memory atomics), a warp scan that finds the bin
+// holding rank k, then -- when that bin holds <= 32 keys, the usual case --
+// the survivors are compacted one per lane and the remaining low bits are
+// bisected with one ballot per bit.  A crowded bin falls back to bisecting
+// the low bits over all keys.  Exact: the same order statistic as warp_select.
+constexpr int kSelBins = 128;
+struct __align__(16) SelScratch {
+    uint32_t hist[kSelBins];  // read as uint4 per lane
+    uint32_t buf[32];
+    uint32_t n, pad[3];
+};
+
+template <int VPL>
+__device__ __forceinline__ uint32_t warp_select_hist(const uint32_t (&v)[VPL], uint32_t lo, uint32_t hi, int k,
+                                                     SelScratch& sc) {
+    const uint32_t range = hi - lo;
+    if (range == 0) return lo;
+    const int nb = 32 - __clz(range);
+    if (nb <= 7) return warp_select<VPL>(v, lo, hi, k);
+    const int shift = nb - 7;
+    const int lane = threadIdx.x & 31;
+    for (int i = lane; i < kSelBins; i += 32) sc.hist[i] = 0;
+    if (lane == 0) sc.n = 0;
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < VPL; ++i)
+        if (v[i] != 0xffffffffu) atomicAdd(&sc.hist[(v[i] - lo) >> shift], 1u);
+    __syncwarp();
+    const uint4 h = reinterpret_cast<const uint4*>(sc.hist)[lane];
+    const uint32_t tot = h.x + h.y + h.z + h.w;
+    uint32_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t excl = incl - tot, uk = (uint32_t)k;
+    const int src = __ffs(__ballot_sync(0xffffffffu, excl <= uk && uk < incl)) - 1;
+    uint32_t bin = 4 * lane, below = excl;
+    if (uk >= below + h.x) {
+        below += h.x;
+        ++bin;
+        if (uk >= below + h.y) {
+            below += h.y;
+            ++bin;
+            if (uk >= below + h.z) {
+                below += h.z;
+                ++bin;
+            }
+        }
+    }
+    bin = __shfl_sync(0xffffffffu, bin, src);
+    below = __shfl_sync(0xffffffffu, below, src);
+    const uint32_t nbin = sc.hist[bin];
+    uint32_t ans = bin << shift;
+    if (nbin <= 32) {
+#pragma unroll
+        for (int i = 0; i < VPL; ++i)
+            if (v[i] != 0xffffffffu && ((v[i] - lo) >> shift) == bin) sc.buf[atomicAdd(&sc.n, 1u)] = v[i] - lo;
+        __syncwarp();
+        const uint32_t sv = (uint32_t)lane < nbin ? sc.buf[lane] : 0xffffffffu;
+        const uint32_t kk = uk - below;
+        for (int b = shift - 1; b >= 0; --b) {
+            const uint32_t cand = ans | (1u << b);
+            if ((uint32_t)__popc(__ballot_sync(0xffffffffu, sv < cand)) <= kk) ans = cand;
+        }
+    } else {
+        uint32_t u[VPL];
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) u[i] = v[i] - lo;
+        for (int b = shift - 1; b >= 0; --b) {
+            const uint32_t cand = ans | (1u << b);
+            uint32_t c = 0;
+#pragma unroll
+            for (int i = 0; i < VPL; ++i) c += (v[i] != 0xffffffffu && u[i] < cand) ? 1u : 0u;
+            c = __reduce_add_sync(0xffffffffu, c);
+            if (c <= uk) ans = cand;
+        }
+    }
+    __syncwarp();  // scratch reused by the next selection
+    return lo + ans;
+}
+
 // max - median over the warp's keys (numpy's midpoint for even counts).
 template <int VPL>
-__device__ __forceinline__ float max_minus_median(const uint32_t (&v)[VPL], uint32_t lo, uint32_t hi, int cnt) {
+__device__ __forceinline__ float max_minus_median(const uint32_t (&v)[VPL], uint32_t lo, uint32_t hi, int cnt,
+                                                  SelScratch& sc) {
     const int mid = cnt / 2;
+    constexpr bool kHist = VPL >= 4;  // histogram select pays off from ~100 keys per warp
+    auto sel = [&](int k) { return kHist ? warp_select_hist<VPL>(v, lo, hi, k, sc) : warp_select<VPL>(v, lo, hi, k); };
     float med;
     if (cnt & 1) {
-        med = fkey_inv(warp_select<VPL>(v, lo, hi, mid));
+        med = fkey_inv(sel(mid));
     } else {
-        const uint32_t a = warp_select<VPL>(v, lo, hi, mid - 1);
+        const uint32_t a = sel(mid - 1);
         uint32_t le = 0, above = 0xffffffffu;
 #pragma unroll
         for (int i = 0; i < VPL; ++i) {
@@ -811,6 +899,7 @@ __device__ __forceinline__ float max_minus_median(const uint32_t (&v)[VPL], uint
 template <int VPL, bool HP>
 __global__ void __launch_bounds__(kK4Threads) median_kernel(K4Args a) {
     extern __shared__ float sm4[];  // [cnt + 2 hh][kK4Pix + 1]
+    __shared__ SelScratch s_sel[kK4Threads / 32];
     constexpr int ST = kK4Pix + 1;
     const int blk = blockIdx.y;
     const int64_t t0 = a.g0 + (int64_t)blk * a.L;
@@ -864,7 +953,7 @@ __global__ void __launch_bounds__(kK4Threads) median_kernel(K4Args a) {
         }
         lo = __reduce_min_sync(0xffffffffu, lo);
         hi = __reduce_max_sync(0xffffffffu, hi);
-        const float r = max_minus_median<VPL>(v, lo, hi, cnt);
+        const float r = max_minus_median<VPL>(v, lo, hi, cnt, s_sel[warp]);
         if (lane == 0) a.temporal[(int64_t)blk * a.hw + p0 + pp] = r;
     }
 }
