@@ -207,17 +207,21 @@ static int choose_group_size(const std::vector<int32_t>& o, int patch, int radiu
 // dy * pitch + col_p mod 32.  Pick the odd pitch in [max_wu, max_wu + 64)
 // with the fewest wavefronts over every warp of every group (ties: smallest).
 static int choose_pitch(const std::vector<PatchGroup>& groups, const std::vector<int32_t>& col, int S,
-                        int max_wu) {
+                        int max_wu, bool split17) {
     int best_pitch = max_wu | 1;
     long long best = -1;
     for (int pitch = max_wu | 1; pitch < max_wu + 64; pitch += 2) {
         long long cost = 0;
         for (const auto& g : groups) {
-            const int items = g.count * S;
+            // lanes -> (patch, candidate row): S rows per patch, or the split
+            // search kernel's 16 lanes per patch over rows {0..16} \ {8}
+            const int per = split17 ? 16 : S;
+            const int items = g.count * per;
             for (int w0 = 0; w0 < items; w0 += 32) {
                 int addr[32], n = 0;
                 for (int it = w0; it < std::min(items, w0 + 32); ++it) {
-                    const int p = it / S, dy = it % S;
+                    const int p = it / per, l = it % per;
+                    const int dy = split17 ? (l < 8 ? l : l + 1) : l;
                     addr[n++] = dy * pitch + col[g.first + p];
                 }
                 int worst = 0;
@@ -301,7 +305,8 @@ int vb_motion_plan_create(vb_motion_plan** out, int height, int width, int patch
         t.max_wu = std::max(t.max_wu, (int)g.wu);
     }
     static const char* force_pitch = getenv("VB_PITCH");  // experiment knob (0 = max_wu | 1)
-    t.pitch = force_pitch ? atoi(force_pitch) : choose_pitch(groups, col, 2 * radius + 1, t.max_wu);
+    t.pitch = force_pitch ? atoi(force_pitch)
+                          : choose_pitch(groups, col, 2 * radius + 1, t.max_wu, patch == 21 && radius == 8);
     if (t.pitch < t.max_wu) t.pitch = t.max_wu | 1;
     cudaError_t e = cudaSuccess;
     e = e ? e : cudaMalloc(&t.tmpl, (size_t)n_origins * patch * t.tp * sizeof(float));

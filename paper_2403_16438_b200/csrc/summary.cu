@@ -908,12 +908,27 @@ __global__ void __launch_bounds__(kK4Threads) median_kernel(K4Args a) {
     const int rows = cnt + 2 * hh;
     const int64_t p0 = (int64_t)blockIdx.x * kK4Pix;
     const int np = (int)((int64_t)kK4Pix < a.hw - p0 ? (int64_t)kK4Pix : a.hw - p0);
-#pragma unroll 8
-    for (int i = threadIdx.x; i < rows * kK4Pix; i += kK4Threads) {
-        const int tt = i / kK4Pix, pp = i - tt * kK4Pix;
-        int64_t g = t0 - hh + tt;
-        if constexpr (HP) g = reflect64(g, a.t_total);
-        sm4[tt * ST + pp] = pp < np ? __ldcs(a.sm + (g - a.s_lo) * a.hw + p0 + pp) : 0.f;
+    // staging: 16 independent loads in flight per thread before their stores
+    // (the phase is latency-bound; each warp row is 2 x 64 contiguous bytes)
+    {
+        constexpr int kB = 16;
+        const int total = rows * kK4Pix;
+        for (int i0 = threadIdx.x; i0 < total; i0 += kB * kK4Threads) {
+            float vals[kB];
+#pragma unroll
+            for (int j = 0; j < kB; ++j) {
+                const int i = i0 + j * kK4Threads;
+                const int tt = i / kK4Pix, pp = i - tt * kK4Pix;
+                int64_t g = t0 - hh + tt;
+                if constexpr (HP) g = reflect64(g, a.t_total);
+                vals[j] = (i < total && pp < np) ? __ldcs(a.sm + (g - a.s_lo) * a.hw + p0 + pp) : 0.f;
+            }
+#pragma unroll
+            for (int j = 0; j < kB; ++j) {
+                const int i = i0 + j * kK4Threads;
+                if (i < total) sm4[(i / kK4Pix) * ST + (i % kK4Pix)] = vals[j];
+            }
+        }
     }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
