@@ -190,6 +190,32 @@ int vb_block_finish(const float* smoothed_dev, int64_t s_lo, int64_t n_smoothed,
                     int64_t t_total, int highpass_window, int height, int width, const double* sum_dev,
                     float* spatial_dev, float* temporal_dev, void* stream);
 
+/* ---------------- summary normalisation + U-Net tiles ----------------
+ * The consumer of the per-block summaries in the reference pipeline
+ * (pipeline.py:222-223).  Parameters are the float32 tensors of
+ * unet.architecture() (unet.py:34-54) flattened in that order (kernel
+ * [cout][cin][k][k] then bias [cout] per conv): vb_unet_param_count() floats. */
+typedef struct vb_unet vb_unet;
+int64_t vb_unet_param_count(void);
+int vb_unet_create(vb_unet** net, const float* params_host, int64_t n_params);
+/* unet.forward_batch (unet.py:154-178): patches_dev float32 [n][2][64][64] ->
+ * probs_dev float32 [n][64][64] (sigmoid outputs). */
+int vb_unet_forward(vb_unet* net, const float* patches_dev, int64_t n, float* probs_dev, void* stream);
+/* unet.normalize_pair (unet.py:186-196) for n_blocks pairs: spatial_dev /
+ * temporal_dev float32 [n_blocks][h][w] -> out_dev float32 [n_blocks][2][h][w]
+ * (numpy "linear" 1st/99th percentiles; a constant channel maps to 0). */
+int vb_normalize_pair(const float* spatial_dev, const float* temporal_dev, int64_t n_blocks, int height, int width,
+                      float* out_dev, void* stream);
+/* unet.tile_and_merge (unet.py:212-245) for n_blocks normalised pairs
+ * [n_blocks][2][h][w] -> prob_dev float32 [n_blocks][h][w]. */
+int vb_unet_tile_merge(vb_unet* net, const float* normalized_dev, int64_t n_blocks, int height, int width, int stride,
+                       float* prob_dev, void* stream);
+/* normalize_pair + tile_and_merge per block (pipeline.py:222-223);
+ * normalized_dev (nullable) receives the normalised pairs. */
+int vb_unet_segment(vb_unet* net, const float* spatial_dev, const float* temporal_dev, int64_t n_blocks, int height,
+                    int width, int stride, float* normalized_dev, float* prob_dev, void* stream);
+int vb_unet_destroy(vb_unet* net);
+
 /* ---------------- whole stage, host buffers (drop-in boundary) ---------------- */
 typedef struct vb_stage_config {
     int height, width;

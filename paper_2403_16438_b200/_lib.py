@@ -65,6 +65,13 @@ SIGNATURES = {
                                _vp, _vp, _vp, _vp]),
     "vb_block_piece": (_i32, [_vp, _i32, _vp, _i64, _i32, _i32, _vp, _i32, _vp, _i64, _i64, _vp, _vp, _vp, _vp]),
     "vb_block_finish": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "vb_unet_param_count": (_i64, []),
+    "vb_unet_create": (_i32, [C.POINTER(_vp), _vp, _i64]),
+    "vb_unet_forward": (_i32, [_vp, _vp, _i64, _vp, _vp]),
+    "vb_normalize_pair": (_i32, [_vp, _vp, _i64, _i32, _i32, _vp, _vp]),
+    "vb_unet_tile_merge": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp]),
+    "vb_unet_segment": (_i32, [_vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp]),
+    "vb_unet_destroy": (_i32, [_vp]),
     "vb_shading_gain": (_i32, [_vp, _i32, _i32, _vp, _i32, _vp, _vp]),
     "vb_correct_frames_ex": (_i32, [_vp, _i32, _i64, _i32, _i32, _vp, _vp, _vp, _vp]),
     "vb_stage_set_highpass": (_i32, [_vp, _i32]),

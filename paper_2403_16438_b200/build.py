@@ -12,7 +12,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libvoltb200.so"
-SOURCES = ["capi.cu", "stage.cu", "motion.cu", "summary.cu", "probe.cu", "traces.cu"]
+SOURCES = ["capi.cu", "stage.cu", "motion.cu", "summary.cu", "probe.cu", "traces.cu", "unet.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-O3",
          f"-I{ROOT / 'include'}"]

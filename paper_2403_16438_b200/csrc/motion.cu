@@ -794,6 +794,8 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     const size_t per_frame_part = (size_t)t.n_groups * SS * sizeof(double);
     const size_t per_frame_inv = (size_t)t.n * SS * sizeof(float);
     int64_t batch = std::max<int64_t>(1, (int64_t)(((size_t)1 << 30) / (per_frame_part + per_frame_inv)));
+    static const char* force_batch = getenv("VB_ZNCC_BATCH");  // experiment knob (frames per stats+search pair)
+    if (force_batch && atoll(force_batch) > 0) batch = atoll(force_batch);
     batch = std::min(batch, n_frames);
     double* partial = nullptr;
     float* inv = nullptr;

@@ -1,0 +1,691 @@
+// Summary normalisation + lightweight U-Net tiles, sm_100a.
+//
+// Reference (paths under /root/reference/pkg/src/voltseg):
+//   normalize_pair   unet.py:186-196  (1st/99th percentiles, numpy "linear"
+//                    method; (x - p1) / (p99 - p1) in float64, clipped, f32)
+//   forward_batch    unet.py:154-178  (enc 16/32/64, two 3x3 conv + ReLU per
+//                    level, 2x2 max-pool, nearest upsample + skip concat,
+//                    1x1 conv + sigmoid; zero padding per 64x64 patch)
+//   tile_and_merge   unet.py:212-245  (64x64 tiles at `stride`, last tile
+//                    flush to the edge, numpy "reflect" pad for small frames,
+//                    tent-weighted float64 blend, clip)
+//
+// B200 design: one CTA computes a 16x16 output tile of one patch for ALL
+// output channels (<= 64 accumulators per thread), staging 8 input channels
+// x 18x18 halo and their [ci][tap][cout] weights in shared memory; weights
+// are read as float4 broadcasts.  Input staging fuses the layer's source:
+// the normalised summary images at the tile origin (first layer, no patch
+// copy), a plain NCHW tensor, or nearest-upsample(low) ++ skip (decoder).
+// Epilogues fuse ReLU, the 2x2 max-pool (warp shuffles) and the final 1x1
+// conv + sigmoid.  FP32 throughout (the reference is float32 numpy; parity
+// target <= 1e-4 absolute, test_acceptance.py:152-163).
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "vb.cuh"
+
+namespace vb {
+
+namespace {
+
+constexpr int kPatch = 64;
+constexpr int kTile = 16;
+constexpr int kCK = 8;  // input channels staged per round
+constexpr int kUThreads = kTile * kTile;
+
+// numpy float32 key order (same as the median's fkey)
+__device__ __forceinline__ uint32_t fkey_u(float f) {
+    const uint32_t u = __float_as_uint(f);
+    return u ^ ((uint32_t)((int32_t)u >> 31) | 0x80000000u);
+}
+__device__ __forceinline__ float fkey_inv_u(uint32_t k) {
+    return __uint_as_float((k & 0x80000000u) ? (k ^ 0x80000000u) : ~k);
+}
+
+struct ConvArgs {
+    int n, h, w, cin, cout;
+    // source of input channels [0, c0): mode 0 NCHW [n][c0][h][w]; mode 1 nearest
+    // upsample of [n][c0][h/2][w/2]; mode 2 image tiles img[c0][ih][iw] at origins
+    const float* x0;
+    int c0, mode;
+    const float* x1;  // channels [c0, cin): skip [n][cin-c0][h][w] (concat) or null
+    const int2* origins;  // mode 2: patch (x, y) origins in the image
+    int ih, iw;
+    int64_t img_stride;  // mode 2: floats between consecutive images (blocks)
+    int tiles_per_img;   // mode 2: patches per image
+    const float* wt;     // [cout][cin][3][3]
+    const float* bias;   // [cout]
+    float* out;          // [n][cout][h][w] or null
+    float* pooled;       // [n][cout][h/2][w/2] or null
+    const float* w1;     // final 1x1 kernel [cout] (cout -> 1) or null
+    const float* b1;     // final 1x1 bias [1]
+    float* prob;         // [n][h][w] sigmoid(1x1) or null
+};
+
+template <int COUT>
+__global__ void __launch_bounds__(kUThreads) conv3x3_kernel(ConvArgs a) {
+    __shared__ float s_in[kCK][kTile + 2][kTile + 2 + 1];
+    __shared__ __align__(16) float s_w[kCK * 9 * COUT];  // [ci][tap][cout]
+    const int tid = threadIdx.x;
+    const int tx = tid % kTile, ty = tid / kTile;
+    const int tiles_x = a.w / kTile;
+    const int tile = blockIdx.x, n = blockIdx.y;
+    const int oy0 = (tile / tiles_x) * kTile, ox0 = (tile % tiles_x) * kTile;
+    float acc[COUT];
+#pragma unroll
+    for (int c = 0; c < COUT; ++c) acc[c] = 0.0f;
+    const int hw = a.h * a.w;
+    for (int c0 = 0; c0 < a.cin; c0 += kCK) {
+        const int nck = min(kCK, a.cin - c0);
+        __syncthreads();
+        // stage the input halo tile (zero padding outside the patch)
+        for (int i = tid; i < kCK * (kTile + 2) * (kTile + 2); i += kUThreads) {
+            const int ci = i / ((kTile + 2) * (kTile + 2));
+            const int r = i % ((kTile + 2) * (kTile + 2));
+            const int yy = r / (kTile + 2), xx = r % (kTile + 2);
+            const int y = oy0 + yy - 1, x = ox0 + xx - 1;
+            float v = 0.0f;
+            const int c = c0 + ci;
+            if (ci < nck && y >= 0 && y < a.h && x >= 0 && x < a.w) {
+                if (c < a.c0) {
+                    if (a.mode == 0) {
+                        v = a.x0[((int64_t)n * a.c0 + c) * hw + y * a.w + x];
+                    } else if (a.mode == 1) {
+                        const int lw = a.w >> 1, lh = a.h >> 1;
+                        v = a.x0[((int64_t)n * a.c0 + c) * lh * lw + (y >> 1) * lw + (x >> 1)];
+                    } else {
+                        const int img = n / a.tiles_per_img;
+                        const int2 o = a.origins[n];
+                        v = a.x0[(int64_t)img * a.img_stride + ((int64_t)c * a.ih + o.y + y) * a.iw + o.x + x];
+                    }
+                } else {
+                    v = a.x1[((int64_t)n * (a.cin - a.c0) + (c - a.c0)) * hw + y * a.w + x];
+                }
+            }
+            s_in[ci][yy][xx] = v;
+        }
+        for (int i = tid; i < kCK * 9 * COUT; i += kUThreads) {
+            const int co = i % COUT, r = i / COUT;
+            const int ci = r / 9, tap = r % 9;
+            s_w[i] = (ci < nck && co < a.cout) ? a.wt[((int64_t)co * a.cin + c0 + ci) * 9 + tap] : 0.0f;
+        }
+        __syncthreads();
+        for (int ci = 0; ci < nck; ++ci) {
+#pragma unroll
+            for (int tap = 0; tap < 9; ++tap) {
+                const float x = s_in[ci][ty + tap / 3][tx + tap % 3];
+                const float4* wv = reinterpret_cast<const float4*>(s_w + (ci * 9 + tap) * COUT);
+#pragma unroll
+                for (int q = 0; q < COUT / 4; ++q) {
+                    const float4 w4 = wv[q];
+                    acc[4 * q] = fmaf(x, w4.x, acc[4 * q]);
+                    acc[4 * q + 1] = fmaf(x, w4.y, acc[4 * q + 1]);
+                    acc[4 * q + 2] = fmaf(x, w4.z, acc[4 * q + 2]);
+                    acc[4 * q + 3] = fmaf(x, w4.w, acc[4 * q + 3]);
+                }
+            }
+        }
+    }
+    const int y = oy0 + ty, x = ox0 + tx;
+#pragma unroll
+    for (int c = 0; c < COUT; ++c) acc[c] = c < a.cout ? fmaxf(__fadd_rn(acc[c], __ldg(a.bias + c)), 0.0f) : 0.0f;
+    if (a.out) {
+#pragma unroll
+        for (int c = 0; c < COUT; ++c)
+            if (c < a.cout) a.out[((int64_t)n * a.cout + c) * hw + y * a.w + x] = acc[c];
+    }
+    if (a.pooled) {  // 2x2 block = lanes {l, l^1, l^16, l^17} (two tile rows per warp)
+        const int ph = a.h >> 1, pw = a.w >> 1;
+#pragma unroll
+        for (int c = 0; c < COUT; ++c) {
+            float m = fmaxf(acc[c], __shfl_xor_sync(0xffffffffu, acc[c], 1));
+            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
+            if (c < a.cout && !(tx & 1) && !(ty & 1))
+                a.pooled[((int64_t)n * a.cout + c) * ph * pw + (y >> 1) * pw + (x >> 1)] = m;
+        }
+    }
+    if (a.prob) {  // final 1x1 conv + sigmoid (unet.py:129-134, :149-150)
+        float s = 0.0f;
+#pragma unroll
+        for (int c = 0; c < COUT; ++c)
+            if (c < a.cout) s = fmaf(acc[c], __ldg(a.w1 + c), s);
+        s = __fadd_rn(s, __ldg(a.b1));
+        a.prob[(int64_t)n * hw + y * a.w + x] = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-s)));
+    }
+}
+
+template <int COUT>
+int launch_conv(const ConvArgs& a, cudaStream_t s) {
+    if (a.h % kTile || a.w % kTile) return fail(VB_EINVAL, "U-Net tile size");
+    dim3 grid((unsigned)((a.h / kTile) * (a.w / kTile)), (unsigned)a.n);
+    {
+        ProfScope ps(kProfOther, s);
+        conv3x3_kernel<COUT><<<grid, kUThreads, 0, s>>>(a);
+    }
+    VB_LAUNCHED();
+    return VB_OK;
+}
+
+int conv(const ConvArgs& a, cudaStream_t s) {
+    if (a.cout <= 16) return launch_conv<16>(a, s);
+    if (a.cout <= 32) return launch_conv<32>(a, s);
+    if (a.cout <= 64) return launch_conv<64>(a, s);
+    return fail(VB_EINVAL, "U-Net layer wider than 64 channels");
+}
+
+// ------------------------------------------------------------- percentiles
+// numpy "linear" quantile (np.percentile default): virtual index
+// n*q + (alpha + q*(1 - alpha - beta)) - 1 with alpha = beta = 1
+// (_compute_virtual_index), neighbours floor / floor + 1 clamped like
+// _get_indexes, gamma = index - floor.
+struct PctIdx {
+    int64_t prev, next;
+    double gamma;
+};
+PctIdx pct_index(int64_t n, double q) {
+    const double vi = (double)n * q + (1.0 + q * (1.0 - 1.0 - 1.0)) - 1.0;
+    PctIdx p;
+    double pv = floor(vi);
+    p.gamma = vi - pv;
+    if (vi >= (double)(n - 1)) {
+        p.prev = p.next = n - 1;
+    } else if (vi < 0) {
+        p.prev = p.next = 0;
+    } else {
+        p.prev = (int64_t)pv;
+        p.next = p.prev + 1;
+    }
+    return p;
+}
+
+struct PctArgs {
+    const float* data;  // channel c at data + c * stride  (c = 2*block + {0: spatial, 1: temporal})
+    const float* data2; // temporal base (channel odd) ; spatial base for even
+    int64_t stride;     // floats between consecutive blocks
+    int64_t n;          // values per channel
+    int64_t rank[4];    // prev/next of p1, prev/next of p99
+    double gamma[2];
+    double* out;        // [2K][3]: p1, p99, constant flag
+};
+
+// One CTA per channel: exact order statistics by 8-bit radix select for the
+// four ranks at once, then numpy's _lerp in float64 (diff of the float32
+// neighbours in float32, as numpy subtracts the two float32 values).
+__global__ void __launch_bounds__(1024) percentile_kernel(PctArgs a) {
+    __shared__ uint32_t hist[4][256];
+    __shared__ uint32_t s_prefix[4], s_rank[4];
+    const int ch = blockIdx.x;
+    const float* x = (ch & 1 ? a.data2 : a.data) + (int64_t)(ch >> 1) * a.stride;
+    if (threadIdx.x < 4) {
+        s_prefix[threadIdx.x] = 0;
+        s_rank[threadIdx.x] = (uint32_t)a.rank[threadIdx.x];
+    }
+    for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 24 - 8 * pass;
+        for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&hist[0][0])[i] = 0;
+        __syncthreads();
+        uint32_t pre[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) pre[j] = s_prefix[j];
+        const uint32_t hmask = pass == 0 ? 0u : (0xffffffffu << (32 - 8 * pass));
+        for (int64_t i = threadIdx.x; i < a.n; i += blockDim.x) {
+            const uint32_t k = fkey_u(x[i]);
+            const uint32_t d = (k >> shift) & 255u;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if ((k & hmask) == pre[j]) atomicAdd(&hist[j][d], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x < 4) {
+            const int j = threadIdx.x;
+            uint32_t r = s_rank[j], c = 0;
+            int d = 0;
+            for (; d < 255; ++d) {
+                if (r < c + hist[j][d]) break;
+                c += hist[j][d];
+            }
+            s_rank[j] = r - c;
+            s_prefix[j] = pre[j] | ((uint32_t)d << shift);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        double p[2];
+        for (int q = 0; q < 2; ++q) {
+            const float lo = fkey_inv_u(s_prefix[2 * q]), hi = fkey_inv_u(s_prefix[2 * q + 1]);
+            const double t = a.gamma[q];
+            const double diff = (double)__fsub_rn(hi, lo);  // float32 subtract (numpy: b - a on f32)
+            double r = (double)lo + diff * t;
+            if (t >= 0.5) r = (double)hi - diff * (1.0 - t);
+            p[q] = r;
+        }
+        a.out[3 * ch] = p[0];
+        a.out[3 * ch + 1] = p[1];
+        a.out[3 * ch + 2] = p[1] <= p[0] ? 1.0 : 0.0;
+    }
+}
+
+// out[b][c][i] = float32(clip((x - p1) / (p99 - p1), 0, 1)) in float64, or 0
+// for a constant channel (unet.py:190-195)
+__global__ void normalize_kernel(const float* __restrict__ sp, const float* __restrict__ tp, int64_t stride,
+                                 int64_t n, int nblk, const double* __restrict__ pct, float* __restrict__ out) {
+    const int64_t total = (int64_t)nblk * 2 * n;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t chn = i / n, j = i - chn * n;
+        const int b = (int)(chn >> 1), c = (int)(chn & 1);
+        const double p1 = pct[3 * chn], p99 = pct[3 * chn + 1];
+        float v = 0.0f;
+        if (pct[3 * chn + 2] == 0.0) {
+            const double x = (double)(c ? tp : sp)[(int64_t)b * stride + j];
+            double r = (x - p1) / (p99 - p1);
+            r = r < 0.0 ? 0.0 : (r > 1.0 ? 1.0 : r);
+            v = (float)r;
+        }
+        out[i] = v;
+    }
+}
+
+// numpy np.pad(..., mode="reflect") index (mirror without repeating the edge)
+__host__ __device__ __forceinline__ int np_reflect(int i, int n) {
+    if (n == 1) return 0;
+    const int period = 2 * (n - 1);
+    int m = i % period;
+    if (m < 0) m += period;
+    return m < n ? m : period - m;
+}
+
+__global__ void pad_kernel(const float* __restrict__ in, int nimg, int h, int w, int ph, int pw,
+                           float* __restrict__ out) {
+    const int64_t total = (int64_t)nimg * ph * pw;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t img = i / ((int64_t)ph * pw);
+        const int r = (int)(i - img * ph * pw);
+        const int y = r / pw, x = r % pw;
+        out[i] = in[img * h * w + (int64_t)np_reflect(y, h) * w + np_reflect(x, w)];
+    }
+}
+
+struct MergeArgs {
+    const float* probs;  // [K * tiles][64][64]
+    const float* tent;   // [64][64]
+    const int* ys;
+    const int* xs;
+    int nys, nxs;
+    int h, w;            // output (cropped)
+    int nblk;
+    float* out;          // [K][h][w]
+};
+
+// Tent-weighted float64 blend in the reference's tile order (unet.py:236-244)
+__global__ void merge_kernel(MergeArgs a) {
+    const int64_t total = (int64_t)a.nblk * a.h * a.w;
+    const int tiles = a.nys * a.nxs;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int b = (int)(i / ((int64_t)a.h * a.w));
+        const int r = (int)(i - (int64_t)b * a.h * a.w);
+        const int y = r / a.w, x = r % a.w;
+        double acc = 0.0, nrm = 0.0;
+        for (int iy = 0; iy < a.nys; ++iy) {
+            const int y0 = a.ys[iy];
+            if (y < y0 || y >= y0 + kPatch) continue;
+            for (int ix = 0; ix < a.nxs; ++ix) {
+                const int x0 = a.xs[ix];
+                if (x < x0 || x >= x0 + kPatch) continue;
+                const int t = (y - y0) * kPatch + (x - x0);
+                const float tw = a.tent[t];
+                const float pv = a.probs[((int64_t)b * tiles + iy * a.nxs + ix) * kPatch * kPatch + t];
+                acc += (double)__fmul_rn(pv, tw);
+                nrm += (double)tw;
+            }
+        }
+        float m = (float)(acc / nrm);
+        m = m < 0.0f ? 0.0f : (m > 1.0f ? 1.0f : m);
+        a.out[i] = m;
+    }
+}
+
+int grid_for(int64_t total) { return (int)std::min<int64_t>((total + 255) / 256, 148 * 16); }
+
+}  // namespace
+
+// Canonical parameter order = unet.architecture() (unet.py:34-54).
+struct UNetLayer {
+    int cin, cout;
+    int64_t kofs, bofs;
+};
+
+}  // namespace vb
+
+using namespace vb;
+
+struct vb_unet {
+    float* params = nullptr;  // device copy, canonical order
+    std::vector<UNetLayer> layers;  // enc1.c1, enc1.c2, enc2.c1, enc2.c2, enc3.c1, enc3.c2, dec2.c1, dec2.c2, dec1.c1, dec1.c2, out
+    float* tent = nullptr;          // [64][64] device
+};
+
+namespace {
+
+int64_t unet_param_count(std::vector<UNetLayer>* layers) {
+    const int widths[3] = {16, 32, 64};
+    std::vector<std::pair<int, int>> convs;  // (cin, cout)
+    int cin = 2;
+    for (int l = 0; l < 3; ++l) {
+        convs.push_back({cin, widths[l]});
+        convs.push_back({widths[l], widths[l]});
+        cin = widths[l];
+    }
+    for (int l = 2; l >= 1; --l) {
+        const int cout = widths[l - 1];
+        convs.push_back({cin + cout, cout});
+        convs.push_back({cout, cout});
+        cin = cout;
+    }
+    int64_t off = 0;
+    for (size_t i = 0; i < convs.size(); ++i) {
+        UNetLayer L{convs[i].first, convs[i].second, off, off + (int64_t)convs[i].first * convs[i].second * 9};
+        off = L.bofs + convs[i].second;
+        if (layers) layers->push_back(L);
+    }
+    UNetLayer out{cin, 1, off, off + cin};
+    off = out.bofs + 1;
+    if (layers) layers->push_back(out);
+    return off;
+}
+
+// unet.py:_tent_weights (float64 ramp outer product, floor 1e-3, float32)
+void tent_host(float* t) {
+    double ramp[kPatch];
+    for (int i = 0; i < kPatch; ++i) ramp[i] = 1.0 - fabs((double)i - (kPatch - 1) / 2.0) / (kPatch / 2.0);
+    for (int y = 0; y < kPatch; ++y)
+        for (int x = 0; x < kPatch; ++x) t[y * kPatch + x] = (float)std::max(ramp[y] * ramp[x], 1e-3);
+}
+
+std::vector<int> tile_positions(int extent, int stride) {  // unet.py:199-203
+    std::vector<int> pos;
+    for (int p = 0; p <= extent - kPatch; p += stride) pos.push_back(p);
+    if (pos.empty() || pos.back() != extent - kPatch) pos.push_back(extent - kPatch);
+    return pos;
+}
+
+// Forward over n patches whose first layer reads `src` per ConvArgs mode 0/2.
+int unet_forward(vb_unet* net, ConvArgs first, int64_t n, float* probs, cudaStream_t s) {
+    if (n <= 0) return VB_OK;
+    const int64_t P2 = (int64_t)kPatch * kPatch;
+    // scratch: e1a e1 p1 e2a e2 p2 e3a e3 d2a d2 d1a (floats per patch)
+    const int64_t sz[11] = {16 * P2, 16 * P2, 16 * P2 / 4, 32 * P2 / 4, 32 * P2 / 4, 32 * P2 / 16,
+                            64 * P2 / 16, 64 * P2 / 16, 32 * P2 / 4, 32 * P2 / 4, 16 * P2};
+    int64_t per = 0;
+    for (int i = 0; i < 11; ++i) per += sz[i];
+    // patches per pass: bound the scratch to ~2 GB
+    int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n, ((int64_t)2 << 30) / (per * 4)));
+    if (first.mode == 2 && chunk < n)  // tile batches start on an image boundary
+        chunk = std::max<int64_t>(first.tiles_per_img, chunk / first.tiles_per_img * first.tiles_per_img);
+    float* scratch = nullptr;
+    keep_pool();
+    VB_CUDA(cudaMallocAsync(&scratch, (size_t)(per * chunk) * sizeof(float), s));
+    float* buf[11];
+    {
+        float* p = scratch;
+        for (int i = 0; i < 11; ++i) {
+            buf[i] = p;
+            p += sz[i] * chunk;
+        }
+    }
+    float *e1a = buf[0], *e1 = buf[1], *p1 = buf[2], *e2a = buf[3], *e2 = buf[4], *p2 = buf[5], *e3a = buf[6],
+          *e3 = buf[7], *d2a = buf[8], *d2 = buf[9], *d1a = buf[10];
+    const float* P = net->params;
+    auto L = [&](int i) { return net->layers[i]; };
+    int rc = VB_OK;
+    for (int64_t n0 = 0; n0 < n && rc == VB_OK; n0 += chunk) {
+        const int nb = (int)std::min<int64_t>(chunk, n - n0);
+        auto base = [&](int li, int h, const float* x0, int c0, int mode, const float* x1, float* out, float* pooled) {
+            ConvArgs a;
+            memset(&a, 0, sizeof(a));
+            a.n = nb;
+            a.h = a.w = h;
+            a.cin = L(li).cin;
+            a.cout = L(li).cout;
+            a.x0 = x0;
+            a.c0 = c0;
+            a.mode = mode;
+            a.x1 = x1;
+            a.wt = P + L(li).kofs;
+            a.bias = P + L(li).bofs;
+            a.out = out;
+            a.pooled = pooled;
+            return a;
+        };
+        ConvArgs a0 = first;
+        a0.n = nb;
+        if (a0.mode == 2) {
+            a0.origins = first.origins + n0;
+            // images advance with the tiles: the kernel derives the image from the patch index
+            // relative to this chunk, so pass the chunk's first image explicitly
+            const int64_t img0 = n0 / first.tiles_per_img;
+            a0.x0 = first.x0 + img0 * first.img_stride;
+            a0.tiles_per_img = first.tiles_per_img;
+            if (n0 % first.tiles_per_img) {  // chunk starts mid-image: fall back to one image per pass
+                rc = fail(VB_EINVAL, "U-Net chunk must start on an image boundary");
+                break;
+            }
+        } else {
+            a0.x0 = first.x0 + n0 * 2 * P2;
+        }
+        a0.h = a0.w = kPatch;
+        a0.cin = L(0).cin;
+        a0.cout = L(0).cout;
+        a0.c0 = L(0).cin;
+        a0.x1 = nullptr;
+        a0.wt = P + L(0).kofs;
+        a0.bias = P + L(0).bofs;
+        a0.out = e1a;
+        a0.pooled = nullptr;
+        a0.prob = nullptr;
+        rc = conv(a0, s);
+        if (!rc) rc = conv(base(1, 64, e1a, 16, 0, nullptr, e1, p1), s);
+        if (!rc) rc = conv(base(2, 32, p1, 16, 0, nullptr, e2a, nullptr), s);
+        if (!rc) rc = conv(base(3, 32, e2a, 32, 0, nullptr, e2, p2), s);
+        if (!rc) rc = conv(base(4, 16, p2, 32, 0, nullptr, e3a, nullptr), s);
+        if (!rc) rc = conv(base(5, 16, e3a, 64, 0, nullptr, e3, nullptr), s);
+        if (!rc) rc = conv(base(6, 32, e3, 64, 1, e2, d2a, nullptr), s);
+        if (!rc) rc = conv(base(7, 32, d2a, 32, 0, nullptr, d2, nullptr), s);
+        if (!rc) rc = conv(base(8, 64, d2, 32, 1, e1, d1a, nullptr), s);
+        if (!rc) {
+            ConvArgs a = base(9, 64, d1a, 16, 0, nullptr, nullptr, nullptr);
+            a.w1 = P + L(10).kofs;
+            a.b1 = P + L(10).bofs;
+            a.prob = probs + n0 * P2;
+            rc = conv(a, s);
+        }
+    }
+    cudaFreeAsync(scratch, s);
+    return rc;
+}
+
+int percentiles(const float* sp, const float* tp, int64_t stride, int64_t n, int64_t nblk, double* pct,
+                cudaStream_t s) {
+    const PctIdx q1 = pct_index(n, 0.01), q99 = pct_index(n, 0.99);  // np.percentile(.., (1, 99)) -> q/100
+    PctArgs a;
+    a.data = sp;
+    a.data2 = tp;
+    a.stride = stride;
+    a.n = n;
+    a.rank[0] = q1.prev;
+    a.rank[1] = q1.next;
+    a.rank[2] = q99.prev;
+    a.rank[3] = q99.next;
+    a.gamma[0] = q1.gamma;
+    a.gamma[1] = q99.gamma;
+    a.out = pct;
+    {
+        ProfScope ps(kProfOther, s);
+        percentile_kernel<<<(unsigned)(2 * nblk), 1024, 0, s>>>(a);
+    }
+    VB_LAUNCHED();
+    return VB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vb_unet_create(vb_unet** out, const float* params_host, int64_t n_params) {
+    if (!out || !params_host) return fail(VB_EINVAL, "null argument");
+    *out = nullptr;
+    auto* net = new vb_unet();
+    const int64_t want = unet_param_count(&net->layers);
+    if (n_params != want) {
+        delete net;
+        return fail(VB_EINVAL, "U-Net parameter count " + std::to_string(n_params) + ", expected " +
+                                   std::to_string(want));
+    }
+    float tent[kPatch * kPatch];
+    tent_host(tent);
+    cudaError_t e = cudaMalloc(&net->params, (size_t)want * sizeof(float));
+    e = e ? e : cudaMalloc(&net->tent, sizeof(tent));
+    e = e ? e : cudaMemcpy(net->params, params_host, (size_t)want * sizeof(float), cudaMemcpyHostToDevice);
+    e = e ? e : cudaMemcpy(net->tent, tent, sizeof(tent), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(net->params);
+        cudaFree(net->tent);
+        delete net;
+        return cuda_fail(e, "vb_unet_create");
+    }
+    *out = net;
+    return VB_OK;
+}
+
+int64_t vb_unet_param_count(void) { return unet_param_count(nullptr); }
+
+int vb_unet_forward(vb_unet* net, const float* patches_dev, int64_t n, float* probs_dev, void* stream) {
+    if (!net || (n > 0 && (!patches_dev || !probs_dev))) return fail(VB_EINVAL, "null argument");
+    ConvArgs a;
+    memset(&a, 0, sizeof(a));
+    a.x0 = patches_dev;
+    a.mode = 0;
+    return unet_forward(net, a, n, probs_dev, (cudaStream_t)stream);
+}
+
+int vb_normalize_pair(const float* spatial_dev, const float* temporal_dev, int64_t n_blocks, int height, int width,
+                      float* out_dev, void* stream) {
+    if (!spatial_dev || !temporal_dev || !out_dev) return fail(VB_EINVAL, "null argument");
+    if (n_blocks < 1 || height < 1 || width < 1) return fail(VB_EINVAL, "empty summary images");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t n = (int64_t)height * width;
+    double* pct = nullptr;
+    keep_pool();
+    VB_CUDA(cudaMallocAsync(&pct, (size_t)n_blocks * 2 * 3 * sizeof(double), s));
+    int rc = percentiles(spatial_dev, temporal_dev, n, n, n_blocks, pct, s);
+    if (rc == VB_OK) {
+        normalize_kernel<<<grid_for(n_blocks * 2 * n), 256, 0, s>>>(spatial_dev, temporal_dev, n, n, (int)n_blocks,
+                                                                     pct, out_dev);
+        launches().fetch_add(1, std::memory_order_relaxed);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) rc = cuda_fail(e, "normalize_kernel");
+    }
+    cudaFreeAsync(pct, s);
+    return rc;
+}
+
+int vb_unet_tile_merge(vb_unet* net, const float* normalized_dev, int64_t n_blocks, int height, int width, int stride,
+                       float* prob_dev, void* stream) {
+    if (!net || !normalized_dev || !prob_dev) return fail(VB_EINVAL, "null argument");
+    if (n_blocks < 1 || height < 1 || width < 1) return fail(VB_EINVAL, "empty summary images");
+    if (stride < 1) return fail(VB_EINVAL, "stride must be >= 1");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int ph = std::max(height, kPatch), pw = std::max(width, kPatch);
+    const std::vector<int> ys = tile_positions(ph, stride), xs = tile_positions(pw, stride);
+    const int tiles = (int)(ys.size() * xs.size());
+    std::vector<int2> org((size_t)n_blocks * tiles);
+    for (int64_t b = 0; b < n_blocks; ++b)
+        for (size_t iy = 0; iy < ys.size(); ++iy)
+            for (size_t ix = 0; ix < xs.size(); ++ix) org[(size_t)b * tiles + iy * xs.size() + ix] = make_int2(xs[ix], ys[iy]);
+    keep_pool();
+    float* padded = nullptr;
+    float* probs = nullptr;
+    int2* d_org = nullptr;
+    int* d_pos = nullptr;
+    const bool pad = ph != height || pw != width;
+    cudaError_t e = cudaSuccess;
+    if (pad) e = cudaMallocAsync(&padded, (size_t)n_blocks * 2 * ph * pw * sizeof(float), s);
+    e = e ? e : cudaMallocAsync(&probs, (size_t)n_blocks * tiles * kPatch * kPatch * sizeof(float), s);
+    e = e ? e : cudaMallocAsync(&d_org, org.size() * sizeof(int2), s);
+    e = e ? e : cudaMallocAsync(&d_pos, (ys.size() + xs.size()) * sizeof(int), s);
+    std::vector<int> pos(ys);
+    pos.insert(pos.end(), xs.begin(), xs.end());
+    e = e ? e : cudaMemcpyAsync(d_org, org.data(), org.size() * sizeof(int2), cudaMemcpyHostToDevice, s);
+    e = e ? e : cudaMemcpyAsync(d_pos, pos.data(), pos.size() * sizeof(int), cudaMemcpyHostToDevice, s);
+    int rc = e == cudaSuccess ? VB_OK : cuda_fail(e, "vb_unet_tile_merge setup");
+    const float* img = normalized_dev;
+    if (rc == VB_OK && pad) {
+        pad_kernel<<<grid_for(n_blocks * 2 * ph * pw), 256, 0, s>>>(normalized_dev, (int)n_blocks * 2, height, width, ph,
+                                                                   pw, padded);
+        launches().fetch_add(1, std::memory_order_relaxed);
+        img = padded;
+    }
+    if (rc == VB_OK) {
+        ConvArgs a;
+        memset(&a, 0, sizeof(a));
+        a.x0 = img;
+        a.mode = 2;
+        a.origins = d_org;
+        a.ih = ph;
+        a.iw = pw;
+        a.img_stride = (int64_t)2 * ph * pw;
+        a.tiles_per_img = tiles;
+        rc = unet_forward(net, a, n_blocks * tiles, probs, s);
+    }
+    if (rc == VB_OK) {
+        MergeArgs m;
+        m.probs = probs;
+        m.tent = net->tent;
+        m.ys = d_pos;
+        m.xs = d_pos + ys.size();
+        m.nys = (int)ys.size();
+        m.nxs = (int)xs.size();
+        m.h = height;
+        m.w = width;
+        m.nblk = (int)n_blocks;
+        m.out = prob_dev;
+        {
+            ProfScope ps(kProfOther, s);
+            merge_kernel<<<grid_for(n_blocks * height * width), 256, 0, s>>>(m);
+        }
+        launches().fetch_add(1, std::memory_order_relaxed);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) rc = cuda_fail(e, "merge_kernel");
+    }
+    if (padded) cudaFreeAsync(padded, s);
+    cudaFreeAsync(probs, s);
+    cudaFreeAsync(d_org, s);
+    cudaFreeAsync(d_pos, s);
+    return rc;
+}
+
+int vb_unet_segment(vb_unet* net, const float* spatial_dev, const float* temporal_dev, int64_t n_blocks, int height,
+                    int width, int stride, float* normalized_dev, float* prob_dev, void* stream) {
+    if (!net || !spatial_dev || !temporal_dev || !prob_dev) return fail(VB_EINVAL, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    float* norm = normalized_dev;
+    keep_pool();
+    if (!norm) VB_CUDA(cudaMallocAsync(&norm, (size_t)n_blocks * 2 * height * width * sizeof(float), s));
+    int rc = vb_normalize_pair(spatial_dev, temporal_dev, n_blocks, height, width, norm, stream);
+    if (rc == VB_OK) rc = vb_unet_tile_merge(net, norm, n_blocks, height, width, stride, prob_dev, stream);
+    if (!normalized_dev) cudaFreeAsync(norm, s);
+    return rc;
+}
+
+int vb_unet_destroy(vb_unet* net) {
+    if (!net) return VB_OK;
+    cudaFree(net->params);
+    cudaFree(net->tent);
+    delete net;
+    return VB_OK;
+}
+
+}  // extern "C"
