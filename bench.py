@@ -45,6 +45,9 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--stage", choices=["preprocess", "unet"], default="preprocess",
+                   help="preprocess: the headline stage; unet: the summaries' consumer (normalize_pair + "
+                        "tile_and_merge for every block, SURVEY 8(f) row 2)")
     p.add_argument("--config", default=CONFIG)
     p.add_argument("--frames", type=int, default=0, help="override frames per rank (profiling only)")
     p.add_argument("--no-e2e", action="store_true")
@@ -464,8 +467,100 @@ def run_ours(args):
     return 0
 
 
+def unet_flops_per_patch() -> float:
+    """2 * MACs of the canonical U-Net on one 64x64 patch (unet.py:34-54, :154-178)."""
+    from paper_2403_16438_b200 import unet
+
+    side = {"enc1": 64, "enc2": 32, "enc3": 16, "dec2": 32, "dec1": 64, "out": 64}
+    total = 0.0
+    for name, shape in unet.architecture():
+        if name.endswith(".kernel"):
+            cout, cin, k, _ = shape
+            total += 2.0 * cout * cin * k * k * side[name.split(".")[0]] ** 2
+    return total
+
+
+def run_unet(args):
+    """Segmentation consumer on C2: all K blocks' summary pairs -> probability maps."""
+    import torch
+
+    from paper_2403_16438_b200 import _lib, stage, synth, unet
+    from paper_2403_16438_b200.unet import _tile_count
+
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    cfg = workload(args.config, args.frames)
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    frames = synth.generate(cfg, dev)
+    scfg = stage.StageConfig(search_radius=cfg.radius, segment_length=cfg.segment_length, ref_frames=cfg.ref_frames)
+    pre = stage.DevicePreprocessor(cfg.height, cfg.width, scfg)
+    res = pre.run(frames)
+    sp, tp = res.spatial.contiguous(), res.temporal.contiguous()
+    del frames
+    k = sp.shape[0]
+    weights = unet.WeightBundle.random(np.random.default_rng(7))
+    net = unet.DeviceUNet(weights)
+    prob = torch.empty_like(sp)
+    tiles = _tile_count(cfg.height, cfg.width, unet.DEFAULT_STRIDE)
+    for _ in range(max(args.warmup, 3)):
+        net.segment_device(sp, tp, out=prob)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(0)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = _lib.launch_count()
+    ev0.record()
+    for _ in range(args.steps):
+        net.segment_device(sp, tp, out=prob)
+    ev1.record()
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    flops = unet_flops_per_patch() * k * tiles
+    p2, p1 = _lib.C.c_double(), _lib.C.c_double()
+    _lib.check(_lib.load().vb_fp32_peak_probe(_lib.C.byref(p2), _lib.C.byref(p1)))
+    peak = max(p2.value, p1.value)
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            from oracle import ref
+            ref.load()
+            import voltseg.unet as R
+            spn, tpn = sp[0].cpu().numpy(), tp[0].cpu().numpy()
+            t0 = time.perf_counter()
+            R.tile_and_merge(weights_ref := R.WeightBundle.random(np.random.default_rng(7)), R.normalize_pair(spn, tpn))
+            dt = time.perf_counter() - t0
+            cpu = {"value": 1.0 / dt, "unit": "summary pairs/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": "one C2 summary pair: voltseg normalize_pair + tile_and_merge (numpy BLAS)"}
+            del weights_ref
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"unavailable": str(exc)}
+    line = {
+        "metric": "summary pairs/s through normalize_pair + U-Net tile_and_merge (SURVEY 8(f) row 2)",
+        "value": k / (ms / 1e3), "unit": "summary pairs/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "none",
+        "vs_baseline": None, "dtype": "f32", "data": "summary pairs of the synthetic C2 recording; random weights",
+        "config": {"workload": f"{cfg.name}: {k} blocks of {cfg.height}x{cfg.width}, {tiles} tiles/block, stride 32",
+                   "patches_per_step": k * tiles},
+        "roofline": {"bound": "fp32", "achieved": flops / (ms / 1e3) / 1e12, "peak": peak, "unit": "TFLOP/s",
+                     "frac": flops / (ms / 1e3) / 1e12 / peak,
+                     "algorithmic": f"{unet_flops_per_patch():.4g} flop/patch x {k * tiles} patches per step"},
+        "cpu_baseline": cpu, "gpu_launches": int(launches), "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    net.close()
+    pre.close()
+    return 0
+
+
 def main():
     args = parse()
+    if args.stage == "unet":
+        return run_unet(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <vector>
 
+#include "tma.cuh"
 #include "vb.cuh"
 
 namespace vb {
@@ -33,9 +34,7 @@ namespace vb {
 namespace {
 
 constexpr int kPatch = 64;
-constexpr int kTile = 16;
 constexpr int kCK = 8;  // input channels staged per round
-constexpr int kUThreads = kTile * kTile;
 
 // numpy float32 key order (same as the median's fkey)
 __device__ __forceinline__ uint32_t fkey_u(float f) {
@@ -66,105 +65,187 @@ struct ConvArgs {
     float* prob;         // [n][h][w] sigmoid(1x1) or null
 };
 
+// Register-blocked tile geometry per output width: every thread owns a
+// horizontal strip of 4 pixels x 16 output channels (64 accumulators); per
+// (input channel, kernel row) it loads the 6 samples its 3 taps x 4 pixels
+// need and 3 x 16 weights (float4 broadcasts, warps are uniform in their
+// channel group): 192 FFMA per 18 shared loads.
+//   COUT 16: 32x32 tile, 1 channel group;  COUT 32: 16x32 tile, 2 groups;
+//   COUT 64: 16x16 tile, 4 groups  -> 256 threads each.
 template <int COUT>
-__global__ void __launch_bounds__(kUThreads) conv3x3_kernel(ConvArgs a) {
-    __shared__ float s_in[kCK][kTile + 2][kTile + 2 + 1];
-    __shared__ __align__(16) float s_w[kCK * 9 * COUT];  // [ci][tap][cout]
+struct ConvGeom {
+    static constexpr int kGroups = COUT / 16;
+    static constexpr int TW = COUT == 64 ? 16 : 32;
+    static constexpr int TH = COUT == 16 ? 32 : 16;
+    static constexpr int kStrips = TW / 4;
+    static constexpr int kPx = TH * kStrips;  // pixel strips per tile
+    static constexpr int kThreads = kPx * kGroups;
+    static constexpr int IW = TW + 2 + 1;     // padded input row
+    static_assert(kThreads == 256, "256 threads per conv CTA");
+};
+
+__device__ __forceinline__ void cp_async4(void* dst, const float* src, bool valid) {
+    // 4-byte global -> shared copy; src-size 0 zero-fills (padding / absent channels)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(valid ? 4 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <int COUT>
+__global__ void __launch_bounds__(256) conv3x3_kernel(ConvArgs a) {
+    using G = ConvGeom<COUT>;
+    // double-buffered stages: chunk k+1's cp.async copies fly while chunk k computes
+    extern __shared__ __align__(16) float conv_smem[];
+    using InTile = float[kCK][G::TH + 2][G::IW];
+    float (*s_w)[kCK * 9 * COUT] = reinterpret_cast<float (*)[kCK * 9 * COUT]>(conv_smem);  // [ci][tap][cout]
+    InTile* s_in = reinterpret_cast<InTile*>(conv_smem + 2 * kCK * 9 * COUT);
     const int tid = threadIdx.x;
-    const int tx = tid % kTile, ty = tid / kTile;
-    const int tiles_x = a.w / kTile;
+    const int cg = tid / G::kPx;          // channel group (warp-uniform)
+    const int g = tid - cg * G::kPx;
+    const int ty = g / G::kStrips, sx = (g % G::kStrips) * 4;
+    const int tiles_x = a.w / G::TW;
     const int tile = blockIdx.x, n = blockIdx.y;
-    const int oy0 = (tile / tiles_x) * kTile, ox0 = (tile % tiles_x) * kTile;
-    float acc[COUT];
+    const int oy0 = (tile / tiles_x) * G::TH, ox0 = (tile % tiles_x) * G::TW;
+    float acc[4][16];
 #pragma unroll
-    for (int c = 0; c < COUT; ++c) acc[c] = 0.0f;
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int c = 0; c < 16; ++c) acc[j][c] = 0.0f;
     const int hw = a.h * a.w;
-    for (int c0 = 0; c0 < a.cin; c0 += kCK) {
+    auto stage = [&](int buf, int c0) {
         const int nck = min(kCK, a.cin - c0);
-        __syncthreads();
-        // stage the input halo tile (zero padding outside the patch)
-        for (int i = tid; i < kCK * (kTile + 2) * (kTile + 2); i += kUThreads) {
-            const int ci = i / ((kTile + 2) * (kTile + 2));
-            const int r = i % ((kTile + 2) * (kTile + 2));
-            const int yy = r / (kTile + 2), xx = r % (kTile + 2);
+        constexpr int kIn = kCK * (G::TH + 2) * (G::TW + 2);
+        for (int i = tid; i < kIn; i += 256) {
+            const int ci = i / ((G::TH + 2) * (G::TW + 2));
+            const int r = i % ((G::TH + 2) * (G::TW + 2));
+            const int yy = r / (G::TW + 2), xx = r % (G::TW + 2);
             const int y = oy0 + yy - 1, x = ox0 + xx - 1;
-            float v = 0.0f;
             const int c = c0 + ci;
-            if (ci < nck && y >= 0 && y < a.h && x >= 0 && x < a.w) {
+            const bool valid = ci < nck && y >= 0 && y < a.h && x >= 0 && x < a.w;
+            const float* src = a.wt;  // any valid address when zero-filling
+            if (valid) {
                 if (c < a.c0) {
                     if (a.mode == 0) {
-                        v = a.x0[((int64_t)n * a.c0 + c) * hw + y * a.w + x];
+                        src = a.x0 + ((int64_t)n * a.c0 + c) * hw + y * a.w + x;
                     } else if (a.mode == 1) {
                         const int lw = a.w >> 1, lh = a.h >> 1;
-                        v = a.x0[((int64_t)n * a.c0 + c) * lh * lw + (y >> 1) * lw + (x >> 1)];
+                        src = a.x0 + ((int64_t)n * a.c0 + c) * lh * lw + (y >> 1) * lw + (x >> 1);
                     } else {
                         const int img = n / a.tiles_per_img;
                         const int2 o = a.origins[n];
-                        v = a.x0[(int64_t)img * a.img_stride + ((int64_t)c * a.ih + o.y + y) * a.iw + o.x + x];
+                        src = a.x0 + (int64_t)img * a.img_stride + ((int64_t)c * a.ih + o.y + y) * a.iw + o.x + x;
                     }
                 } else {
-                    v = a.x1[((int64_t)n * (a.cin - a.c0) + (c - a.c0)) * hw + y * a.w + x];
+                    src = a.x1 + ((int64_t)n * (a.cin - a.c0) + (c - a.c0)) * hw + y * a.w + x;
                 }
             }
-            s_in[ci][yy][xx] = v;
+            cp_async4(&s_in[buf][ci][yy][xx], src, valid);
         }
-        for (int i = tid; i < kCK * 9 * COUT; i += kUThreads) {
+        for (int i = tid; i < kCK * 9 * COUT; i += 256) {
             const int co = i % COUT, r = i / COUT;
             const int ci = r / 9, tap = r % 9;
-            s_w[i] = (ci < nck && co < a.cout) ? a.wt[((int64_t)co * a.cin + c0 + ci) * 9 + tap] : 0.0f;
+            const bool valid = ci < nck && co < a.cout;
+            cp_async4(&s_w[buf][i], valid ? a.wt + ((int64_t)co * a.cin + c0 + ci) * 9 + tap : a.wt, valid);
+        }
+        cp_async_commit();
+    };
+    stage(0, 0);
+    int buf = 0;
+    for (int c0 = 0; c0 < a.cin; c0 += kCK, buf ^= 1) {
+        const int nck = min(kCK, a.cin - c0);
+        if (c0 + kCK < a.cin) {
+            stage(buf ^ 1, c0 + kCK);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
         __syncthreads();
         for (int ci = 0; ci < nck; ++ci) {
 #pragma unroll
-            for (int tap = 0; tap < 9; ++tap) {
-                const float x = s_in[ci][ty + tap / 3][tx + tap % 3];
-                const float4* wv = reinterpret_cast<const float4*>(s_w + (ci * 9 + tap) * COUT);
+            for (int ky = 0; ky < 3; ++ky) {
+                float xin[6];
 #pragma unroll
-                for (int q = 0; q < COUT / 4; ++q) {
-                    const float4 w4 = wv[q];
-                    acc[4 * q] = fmaf(x, w4.x, acc[4 * q]);
-                    acc[4 * q + 1] = fmaf(x, w4.y, acc[4 * q + 1]);
-                    acc[4 * q + 2] = fmaf(x, w4.z, acc[4 * q + 2]);
-                    acc[4 * q + 3] = fmaf(x, w4.w, acc[4 * q + 3]);
+                for (int j = 0; j < 6; ++j) xin[j] = s_in[buf][ci][ty + ky][sx + j];
+#pragma unroll
+                for (int kx = 0; kx < 3; ++kx) {
+                    const float4* wv = reinterpret_cast<const float4*>(&s_w[buf][(ci * 9 + ky * 3 + kx) * COUT + cg * 16]);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const float4 w4 = wv[q];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const float xv = xin[j + kx];
+                            acc[j][4 * q] = fmaf(xv, w4.x, acc[j][4 * q]);
+                            acc[j][4 * q + 1] = fmaf(xv, w4.y, acc[j][4 * q + 1]);
+                            acc[j][4 * q + 2] = fmaf(xv, w4.z, acc[j][4 * q + 2]);
+                            acc[j][4 * q + 3] = fmaf(xv, w4.w, acc[j][4 * q + 3]);
+                        }
+                    }
                 }
             }
         }
+        __syncthreads();  // buffer `buf` is restaged two chunks later
     }
-    const int y = oy0 + ty, x = ox0 + tx;
+    const int y = oy0 + ty, x = ox0 + sx;
 #pragma unroll
-    for (int c = 0; c < COUT; ++c) acc[c] = c < a.cout ? fmaxf(__fadd_rn(acc[c], __ldg(a.bias + c)), 0.0f) : 0.0f;
+    for (int c = 0; c < 16; ++c) {
+        const int co = cg * 16 + c;
+        const float b = co < a.cout ? __ldg(a.bias + co) : 0.0f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j][c] = co < a.cout ? fmaxf(__fadd_rn(acc[j][c], b), 0.0f) : 0.0f;
+    }
     if (a.out) {
 #pragma unroll
-        for (int c = 0; c < COUT; ++c)
-            if (c < a.cout) a.out[((int64_t)n * a.cout + c) * hw + y * a.w + x] = acc[c];
-    }
-    if (a.pooled) {  // 2x2 block = lanes {l, l^1, l^16, l^17} (two tile rows per warp)
-        const int ph = a.h >> 1, pw = a.w >> 1;
-#pragma unroll
-        for (int c = 0; c < COUT; ++c) {
-            float m = fmaxf(acc[c], __shfl_xor_sync(0xffffffffu, acc[c], 1));
-            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
-            if (c < a.cout && !(tx & 1) && !(ty & 1))
-                a.pooled[((int64_t)n * a.cout + c) * ph * pw + (y >> 1) * pw + (x >> 1)] = m;
+        for (int c = 0; c < 16; ++c) {
+            const int co = cg * 16 + c;
+            if (co < a.cout)
+                *reinterpret_cast<float4*>(a.out + ((int64_t)n * a.cout + co) * hw + y * a.w + x) =
+                    make_float4(acc[0][c], acc[1][c], acc[2][c], acc[3][c]);
         }
     }
-    if (a.prob) {  // final 1x1 conv + sigmoid (unet.py:129-134, :149-150)
-        float s = 0.0f;
+    if (a.pooled) {  // 2x2 blocks: pixel pairs inside the strip, row pairs = lanes l, l ^ kStrips
+        const int ph = a.h >> 1, pw = a.w >> 1;
 #pragma unroll
-        for (int c = 0; c < COUT; ++c)
-            if (c < a.cout) s = fmaf(acc[c], __ldg(a.w1 + c), s);
-        s = __fadd_rn(s, __ldg(a.b1));
-        a.prob[(int64_t)n * hw + y * a.w + x] = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-s)));
+        for (int c = 0; c < 16; ++c) {
+            float m0 = fmaxf(acc[0][c], acc[1][c]), m1 = fmaxf(acc[2][c], acc[3][c]);
+            m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, G::kStrips));
+            m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, G::kStrips));
+            const int co = cg * 16 + c;
+            if (co < a.cout && !(ty & 1))
+                *reinterpret_cast<float2*>(a.pooled + ((int64_t)n * a.cout + co) * ph * pw + (y >> 1) * pw + (x >> 1)) =
+                    make_float2(m0, m1);
+        }
+    }
+    if (a.prob) {  // final 1x1 conv + sigmoid (unet.py:129-134, :149-150); COUT 16 = one group
+        float4 pv;
+        float* pp = &pv.x;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            float sum = 0.0f;
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+                if (c < a.cout) sum = fmaf(acc[j][c], __ldg(a.w1 + c), sum);
+            sum = __fadd_rn(sum, __ldg(a.b1));
+            pp[j] = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-sum)));
+        }
+        *reinterpret_cast<float4*>(a.prob + (int64_t)n * hw + y * a.w + x) = pv;
     }
 }
 
 template <int COUT>
 int launch_conv(const ConvArgs& a, cudaStream_t s) {
-    if (a.h % kTile || a.w % kTile) return fail(VB_EINVAL, "U-Net tile size");
-    dim3 grid((unsigned)((a.h / kTile) * (a.w / kTile)), (unsigned)a.n);
+    using G = ConvGeom<COUT>;
+    if (a.h % G::TH || a.w % G::TW) return fail(VB_EINVAL, "U-Net tile size");
+    if (a.prob && COUT != 16) return fail(VB_EINVAL, "fused output conv needs one channel group");
+    dim3 grid((unsigned)((a.h / G::TH) * (a.w / G::TW)), (unsigned)a.n);
+    const size_t smem = sizeof(float) * 2 * ((size_t)kCK * 9 * COUT + (size_t)kCK * (G::TH + 2) * G::IW);
+    VB_CUDA(cudaFuncSetAttribute(conv3x3_kernel<COUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     {
         ProfScope ps(kProfOther, s);
-        conv3x3_kernel<COUT><<<grid, kUThreads, 0, s>>>(a);
+        conv3x3_kernel<COUT><<<grid, 256, smem, s>>>(a);
     }
     VB_LAUNCHED();
     return VB_OK;
@@ -366,7 +447,30 @@ struct vb_unet {
     float* params = nullptr;  // device copy, canonical order
     std::vector<UNetLayer> layers;  // enc1.c1, enc1.c2, enc2.c1, enc2.c2, enc3.c1, enc3.c2, dec2.c1, dec2.c2, dec1.c1, dec1.c2, out
     float* tent = nullptr;          // [64][64] device
+    // activation scratch owned by the handle, grown on demand (a per-call
+    // stream-ordered allocation of ~1.6 GB was measured to cost up to 190 ms
+    // when the pool had to remap after other large allocations); one call at
+    // a time per handle
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
 };
+
+namespace vb {
+namespace {
+int net_scratch(vb_unet* net, size_t bytes, cudaStream_t s, void** out) {
+    if (bytes > net->scratch_bytes) {
+        VB_CUDA(cudaStreamSynchronize(s));  // the old buffer may still be in use by queued work
+        cudaFree(net->scratch);
+        net->scratch = nullptr;
+        net->scratch_bytes = 0;
+        VB_CUDA(cudaMalloc(&net->scratch, bytes));
+        net->scratch_bytes = bytes;
+    }
+    *out = net->scratch;
+    return VB_OK;
+}
+}  // namespace
+}  // namespace vb
 
 namespace {
 
@@ -426,8 +530,12 @@ int unet_forward(vb_unet* net, ConvArgs first, int64_t n, float* probs, cudaStre
     if (first.mode == 2 && chunk < n)  // tile batches start on an image boundary
         chunk = std::max<int64_t>(first.tiles_per_img, chunk / first.tiles_per_img * first.tiles_per_img);
     float* scratch = nullptr;
-    keep_pool();
-    VB_CUDA(cudaMallocAsync(&scratch, (size_t)(per * chunk) * sizeof(float), s));
+    {
+        void* p = nullptr;
+        const int rc0 = net_scratch(net, (size_t)(per * chunk) * sizeof(float), s, &p);
+        if (rc0) return rc0;
+        scratch = static_cast<float*>(p);
+    }
     float* buf[11];
     {
         float* p = scratch;
@@ -503,7 +611,6 @@ int unet_forward(vb_unet* net, ConvArgs first, int64_t n, float* probs, cudaStre
             rc = conv(a, s);
         }
     }
-    cudaFreeAsync(scratch, s);
     return rc;
 }
 
@@ -684,6 +791,7 @@ int vb_unet_destroy(vb_unet* net) {
     if (!net) return VB_OK;
     cudaFree(net->params);
     cudaFree(net->tent);
+    cudaFree(net->scratch);
     delete net;
     return VB_OK;
 }

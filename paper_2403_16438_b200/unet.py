@@ -193,6 +193,15 @@ def _device_net(weights: WeightBundle) -> DeviceUNet:
     return net
 
 
+def _tile_count(height: int, width: int, stride: int = DEFAULT_STRIDE) -> int:
+    """Patches tile_and_merge runs on one (height, width) image (unet.py:199-203, :223-227)."""
+    def n(extent):
+        extent = max(extent, PATCH)
+        k = len(range(0, extent - PATCH + 1, stride))
+        return k + (0 if (k - 1) * stride == extent - PATCH else 1)
+    return n(height) * n(width)
+
+
 def _f32_device(a) -> torch.Tensor:
     dev = D.require_cuda()
     if isinstance(a, torch.Tensor):
