@@ -253,6 +253,16 @@ int vb_stage_set_shading(vb_stage* stage, const double* weights, int wradius);
 int64_t vb_stage_last_launches(const vb_stage* stage);
 int vb_stage_destroy(vb_stage* stage);
 
+/* Pipeline orchestration (SURVEY 8(f) rows 2 + 4; pipeline.py:190-258 minus
+ * the footprint stage): attach a U-Net (not owned; NULL detaches) and run
+ * correct_motion + summarize + normalize_pair + tile_and_merge per block.  Each
+ * chunk's blocks are segmented on a separate stream while the next chunk's
+ * motion search runs; prob_host: float32 [ceil(n/L)][h][w]. */
+int vb_stage_set_unet(vb_stage* stage, vb_unet* net, int stride);
+int vb_stage_run_host_segment(vb_stage* stage, const void* frames_host, int dtype, int64_t n_frames,
+                              vb_motion* vectors_host, float* spatial_host, float* temporal_host, float* prob_host,
+                              float* corrected_host, float* corrected_dev);
+
 /* Use an externally built template (e.g. all-reduced across ranks) for the
  * following runs instead of averaging the first ref_frames frames of the
  * input (phase A).  ref_dev: device float32 [h][w], copied; NULL restores the

@@ -80,6 +80,8 @@ SIGNATURES = {
     "vb_stage_set_weights": (_i32, [_vp, _vp, _i32]),
     "vb_stage_run_host": (_i32, [_vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _vp]),
     "vb_stage_last_launches": (_i64, [_vp]),
+    "vb_stage_set_unet": (_i32, [_vp, _vp, _i32]),
+    "vb_stage_run_host_segment": (_i32, [_vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "vb_stage_destroy": (_i32, [_vp]),
     "vb_stage_set_reference": (_i32, [_vp, _vp]),
     "vb_launch_count": (_i64, []),

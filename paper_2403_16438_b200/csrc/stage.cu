@@ -53,6 +53,15 @@ struct vb_stage {
     int64_t cap = 0;  // frames per ring slot (chunk + high-pass halo)
     cudaEvent_t ev_h2d[2]{}, ev_comp[2]{}, ev_d2h[2]{};
     int64_t last_launches = 0;
+    // SURVEY 8(f) rows 2 + 4: per-block U-Net segmentation of each chunk's
+    // summaries on its own stream (overlapping the next chunk's motion search),
+    // probability maps drained with the other outputs
+    vb_unet* unet = nullptr;
+    int unet_stride = 32;
+    cudaStream_t s_seg = nullptr;
+    cudaEvent_t ev_seg[2]{};
+    float* d_prob[2] = {nullptr, nullptr};
+    float* h_prob[2] = {nullptr, nullptr};
 };
 
 static void stage_free_buffers(vb_stage* st) {
@@ -67,6 +76,9 @@ static void stage_free_buffers(vb_stage* st) {
         cudaFreeHost(st->h_sp[i]);
         cudaFreeHost(st->h_tp[i]);
         cudaFreeHost(st->h_corr[i]);
+        cudaFree(st->d_prob[i]);
+        cudaFreeHost(st->h_prob[i]);
+        st->d_prob[i] = st->h_prob[i] = nullptr;
         st->d_frames[i] = st->h_stage[i] = nullptr;
         st->h_vec[i] = nullptr;
         st->h_sp[i] = st->h_tp[i] = st->h_corr[i] = nullptr;
@@ -185,8 +197,42 @@ int vb_stage_set_shading(vb_stage* st, const double* weights, int wradius) {
 
 int64_t vb_stage_last_launches(const vb_stage* st) { return st ? st->last_launches : 0; }
 
+int vb_stage_set_unet(vb_stage* st, vb_unet* net, int stride) {
+    if (!st) return fail(VB_EINVAL, "null argument");
+    if (net && stride < 1) return fail(VB_EINVAL, "stride must be >= 1");
+    VB_CUDA(cudaSetDevice(st->cfg.device));
+    if (net && !st->s_seg) {
+        VB_CUDA(cudaStreamCreateWithFlags(&st->s_seg, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) VB_CUDA(cudaEventCreateWithFlags(&st->ev_seg[i], cudaEventDisableTiming));
+    }
+    st->unet = net;
+    st->unet_stride = stride;
+    return VB_OK;
+}
+
+static int stage_run(vb_stage* st, const void* frames_host, int dtype, int64_t n_frames, vb_motion* vectors_host,
+                     float* spatial_host, float* temporal_host, float* prob_host, float* corrected_host,
+                     float* corrected_dev);
+
 int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t n_frames, vb_motion* vectors_host,
                       float* spatial_host, float* temporal_host, float* corrected_host, float* corrected_dev) {
+    return stage_run(st, frames_host, dtype, n_frames, vectors_host, spatial_host, temporal_host, nullptr,
+                     corrected_host, corrected_dev);
+}
+
+int vb_stage_run_host_segment(vb_stage* st, const void* frames_host, int dtype, int64_t n_frames,
+                              vb_motion* vectors_host, float* spatial_host, float* temporal_host, float* prob_host,
+                              float* corrected_host, float* corrected_dev) {
+    if (!st) return fail(VB_EINVAL, "null argument");
+    if (!st->unet) return fail(VB_EINVAL, "no U-Net attached (vb_stage_set_unet)");
+    if (!prob_host) return fail(VB_EINVAL, "null argument");
+    return stage_run(st, frames_host, dtype, n_frames, vectors_host, spatial_host, temporal_host, prob_host,
+                     corrected_host, corrected_dev);
+}
+
+static int stage_run(vb_stage* st, const void* frames_host, int dtype, int64_t n_frames, vb_motion* vectors_host,
+                     float* spatial_host, float* temporal_host, float* prob_host, float* corrected_host,
+                     float* corrected_dev) {
     if (!st || !frames_host || !vectors_host || !spatial_host || !temporal_host) return fail(VB_EINVAL, "null argument");
     if (dtype != VB_U16 && dtype != VB_F32) return fail(VB_EINVAL, "unsupported sample type");
     const vb_stage_config& c = st->cfg;
@@ -209,8 +255,9 @@ int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t 
 
     // (re)allocate the two-slot ring
     const bool ring_corr = corrected_host && !corrected_dev;  // corrected chunks need ring buffers
+    const bool seg = prob_host != nullptr;
     if (st->esz != esz || st->cap < cap || (ring_corr && !st->d_corr[0]) || (corrected_host && !st->h_corr[0]) ||
-        (!pinned && !st->h_stage[0])) {
+        (!pinned && !st->h_stage[0]) || (seg && !st->d_prob[0])) {
         stage_free_buffers(st);
         cudaError_t e = cudaSuccess;
         for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
@@ -225,6 +272,10 @@ int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t 
             if (corrected_host)
                 e = e ? e : cudaHostAlloc(&st->h_corr[i], (size_t)C * hw * sizeof(float), cudaHostAllocDefault);
             if (!pinned) e = e ? e : cudaHostAlloc(&st->h_stage[i], (size_t)cap * hw * esz, cudaHostAllocDefault);
+            if (seg) {
+                e = e ? e : cudaMalloc(&st->d_prob[i], (size_t)cblk * hw * sizeof(float));
+                e = e ? e : cudaHostAlloc(&st->h_prob[i], (size_t)cblk * hw * sizeof(float), cudaHostAllocDefault);
+            }
         }
         if (e != cudaSuccess) {
             stage_free_buffers(st);
@@ -306,6 +357,7 @@ int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t 
         memcpy(temporal_host + (size_t)b0 * hw, st->h_tp[slot], (size_t)nb * hw * sizeof(float));
         if (corrected_host)
             memcpy(corrected_host + (size_t)f0 * hw, st->h_corr[slot], (size_t)nf * hw * sizeof(float));
+        if (seg) memcpy(prob_host + (size_t)b0 * hw, st->h_prob[slot], (size_t)nb * hw * sizeof(float));
         return VB_OK;
     };
     for (int64_t k = 0; k < nchunks && rc == VB_OK; ++k) {
@@ -332,6 +384,14 @@ int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t 
                                  st->weights.data(), st->wradius, so, corr, st->d_sp[slot], st->d_tp[slot], st->s_comp);
         if (rc) break;
         VB_CUDA(cudaEventRecord(st->ev_comp[slot], st->s_comp));
+        if (seg) {  // U-Net of this chunk's blocks overlaps the next chunk's search
+            VB_CUDA(cudaStreamWaitEvent(st->s_seg, st->ev_comp[slot], 0));
+            rc = vb_unet_segment(st->unet, st->d_sp[slot], st->d_tp[slot], nb, c.height, c.width, st->unet_stride,
+                                 nullptr, st->d_prob[slot], st->s_seg);
+            if (rc) break;
+            VB_CUDA(cudaEventRecord(st->ev_seg[slot], st->s_seg));
+            VB_CUDA(cudaStreamWaitEvent(st->s_d2h, st->ev_seg[slot], 0));
+        }
         VB_CUDA(cudaStreamWaitEvent(st->s_d2h, st->ev_comp[slot], 0));
         VB_CUDA(cudaMemcpyAsync(st->h_vec[slot], st->d_vec[slot] + (f0 - a0), (size_t)nf * sizeof(vb_motion),
                                 cudaMemcpyDeviceToHost, st->s_d2h));
@@ -342,6 +402,9 @@ int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t 
         if (corrected_host)
             VB_CUDA(cudaMemcpyAsync(st->h_corr[slot], corr, (size_t)nf * hw * sizeof(float),
                                     cudaMemcpyDeviceToHost, st->s_d2h));
+        if (seg)
+            VB_CUDA(cudaMemcpyAsync(st->h_prob[slot], st->d_prob[slot], (size_t)nb * hw * sizeof(float),
+                                    cudaMemcpyDeviceToHost, st->s_d2h));
         VB_CUDA(cudaEventRecord(st->ev_d2h[slot], st->s_d2h));
         if (k >= 1) rc = drain(k - 1);
     }
@@ -349,8 +412,9 @@ int vb_stage_run_host(vb_stage* st, const void* frames_host, int dtype, int64_t 
     cudaError_t e1 = cudaStreamSynchronize(st->s_h2d);
     cudaError_t e2 = cudaStreamSynchronize(st->s_comp);
     cudaError_t e3 = cudaStreamSynchronize(st->s_d2h);
+    cudaError_t e4 = st->s_seg ? cudaStreamSynchronize(st->s_seg) : cudaSuccess;
     if (rc == VB_OK) {
-        cudaError_t e = e1 ? e1 : (e2 ? e2 : e3);
+        cudaError_t e = e1 ? e1 : (e2 ? e2 : (e3 ? e3 : e4));
         if (e != cudaSuccess) rc = cuda_fail(e, "vb_stage_run_host");
     }
     st->last_launches = launches().load() - launches0;
@@ -373,6 +437,12 @@ int vb_stage_destroy(vb_stage* st) {
     if (st->s_comp) cudaStreamDestroy(st->s_comp);
     if (st->s_h2d) cudaStreamDestroy(st->s_h2d);
     if (st->s_d2h) cudaStreamDestroy(st->s_d2h);
+    if (st->s_seg) {
+        cudaStreamSynchronize(st->s_seg);
+        cudaStreamDestroy(st->s_seg);
+    }
+    for (int i = 0; i < 2; ++i)
+        if (st->ev_seg[i]) cudaEventDestroy(st->ev_seg[i]);
     delete st;
     return VB_OK;
 }

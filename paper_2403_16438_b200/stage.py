@@ -227,6 +227,33 @@ class HostStage:
         _lib.call("vb_stage_run_host", self._h, frames_ptr, dtype, t, p(vec), p(sp), p(tp), p(corr),
                   D.ptr(corrected_dev))
 
+    def attach_unet(self, net, stride: int = 32) -> None:
+        """Segment every block's summaries with `net` (unet.DeviceUNet or a
+        WeightBundle) inside run(..., segment=True) -- SURVEY 8(f) rows 2 + 4."""
+        from . import unet as U
+
+        if net is not None and not isinstance(net, U.DeviceUNet):
+            net = U.DeviceUNet(net)
+        self._net = net
+        _lib.call("vb_stage_set_unet", self._h, net.handle if net is not None else None, int(stride))
+
+    def run_segment(self, frames: np.ndarray, corrected: bool = False):
+        """run() plus the per-block probability maps [K,H,W] (needs attach_unet)."""
+        a = np.ascontiguousarray(frames)
+        if a.dtype not in (np.uint16, np.float32):
+            a = a.astype(np.float32)
+        dtype = _lib.VB_U16 if a.dtype == np.uint16 else _lib.VB_F32
+        t = a.shape[0]
+        k = math.ceil(t / self.cfg.segment_length)
+        vec = np.empty(t, dtype=_lib.MOTION_DTYPE)
+        sp = np.empty((k, self.height, self.width), np.float32)
+        tp = np.empty_like(sp)
+        prob = np.empty_like(sp)
+        corr = np.empty((t, self.height, self.width), np.float32) if corrected else None
+        _lib.call("vb_stage_run_host_segment", self._h, a.ctypes.data, dtype, t, vec.ctypes.data, sp.ctypes.data,
+                  tp.ctypes.data, prob.ctypes.data, corr.ctypes.data if corr is not None else None, None)
+        return vec, sp, tp, prob, corr
+
     @property
     def last_launches(self) -> int:
         return int(_lib.load().vb_stage_last_launches(self._h))
