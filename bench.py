@@ -45,7 +45,7 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--stage", choices=["preprocess", "unet"], default="preprocess",
+    p.add_argument("--stage", choices=["preprocess", "unet", "pipeline"], default="preprocess",
                    help="preprocess: the headline stage; unet: the summaries' consumer (normalize_pair + "
                         "tile_and_merge for every block, SURVEY 8(f) row 2)")
     p.add_argument("--config", default=CONFIG)
@@ -557,10 +557,72 @@ def run_unet(args):
     return 0
 
 
+def run_pipeline(args):
+    """pipeline.py:190-258 without footprints, end to end through the C ABI:
+    pinned uint16 host recording -> vectors, summaries and probability maps on
+    the host (vb_stage_run_host_segment), against the stage alone."""
+    import torch
+
+    from paper_2403_16438_b200 import _lib, stage, synth, unet
+
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    cfg = workload(args.config, args.frames)
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    host = synth.generate(cfg, dev).view(torch.int16).cpu().pin_memory()
+    t = host.shape[0]
+    scfg = stage.StageConfig(search_radius=cfg.radius, segment_length=cfg.segment_length, ref_frames=cfg.ref_frames)
+    hs = stage.HostStage(cfg.height, cfg.width, scfg)
+    net = unet.DeviceUNet(unet.WeightBundle.random(np.random.default_rng(7)))
+    hs.attach_unet(net)
+    k = math.ceil(t / cfg.segment_length)
+    vec = np.empty(t, dtype=_lib.MOTION_DTYPE)
+    sp = np.empty((k, cfg.height, cfg.width), np.float32)
+    tp, prob = np.empty_like(sp), np.empty_like(sp)
+
+    def seg_step():
+        _lib.call("vb_stage_run_host_segment", hs._h, host.data_ptr(), _lib.VB_U16, t, vec.ctypes.data,
+                  sp.ctypes.data, tp.ctypes.data, prob.ctypes.data, None, None)
+
+    def stage_step():
+        hs.run_into(host.data_ptr(), _lib.VB_U16, t, vec, sp, tp)
+
+    out = {}
+    for name, fn in (("pipeline", seg_step), ("stage_only", stage_step)):
+        for _ in range(max(args.warmup, 1)):
+            fn()
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        for _ in range(args.steps):
+            fn()
+        torch.cuda.synchronize()
+        out[name] = t * args.steps / (time.perf_counter() - w0)
+    line = {
+        "metric": "frames/s through motion correction + summaries + U-Net segmentation (pipeline.py:190-258 "
+                  "minus footprints), host in / host out",
+        "value": out["pipeline"], "unit": "frames/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "higher_is_better": True, "scaling": "none", "vs_baseline": None, "dtype": "f32/f64",
+        "data": "synthetic C2 recording (paper_2403_16438_b200.synth); random U-Net weights",
+        "config": {"workload": f"{cfg.name}: {t}x{cfg.height}x{cfg.width} uint16, L={cfg.segment_length}, "
+                               f"{k} blocks segmented", "path": "vb_stage_run_host_segment (C ABI), pinned input"},
+        "stage_only_fps": out["stage_only"],
+        "e2e": {"value": out["pipeline"], "unit": "frames/s", "h2d_bytes_per_step": int(t * cfg.height * cfg.width * 2),
+                "d2h_bytes_per_step": int(t * 32 + 3 * k * cfg.height * cfg.width * 4)},
+    }
+    print(json.dumps(line), flush=True)
+    hs.close()
+    net.close()
+    return 0
+
+
 def main():
     args = parse()
     if args.stage == "unet":
         return run_unet(args)
+    if args.stage == "pipeline":
+        return run_pipeline(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

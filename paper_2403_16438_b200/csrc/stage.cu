@@ -365,7 +365,7 @@ static int stage_run(vb_stage* st, const void* frames_host, int dtype, int64_t n
         const int64_t f0 = k * C, nf = std::min<int64_t>(C, n_frames - f0);
         const int64_t nb = (nf + L - 1) / L;
         const auto [a0, a1] = avail(f0, nf);
-        if (!(k == 0 && chunk0_resident)) rc = upload(slot, a0, a1 - a0);
+        if (k == 0 && !chunk0_resident) rc = upload(slot, a0, a1 - a0);  // later chunks are prefetched below
         if (rc) break;
         VB_CUDA(cudaStreamWaitEvent(st->s_comp, st->ev_h2d[slot], 0));
         VB_CUDA(cudaStreamWaitEvent(st->s_comp, st->ev_d2h[slot], 0));  // outputs of chunk k-2 drained
@@ -406,6 +406,15 @@ static int stage_run(vb_stage* st, const void* frames_host, int dtype, int64_t n
             VB_CUDA(cudaMemcpyAsync(st->h_prob[slot], st->d_prob[slot], (size_t)nb * hw * sizeof(float),
                                     cudaMemcpyDeviceToHost, st->s_d2h));
         VB_CUDA(cudaEventRecord(st->ev_d2h[slot], st->s_d2h));
+        // prefetch chunk k+1 into the other slot before blocking on chunk k-1's
+        // outputs: the H2D stream only waits (device side) for chunk k-1's
+        // compute, so the PCIe copy never waits for the host thread
+        if (k + 1 < nchunks) {
+            const int64_t g0 = (k + 1) * C, gn = std::min<int64_t>(C, n_frames - g0);
+            const auto [b0, b1] = avail(g0, gn);
+            rc = upload(slot ^ 1, b0, b1 - b0);
+            if (rc) break;
+        }
         if (k >= 1) rc = drain(k - 1);
     }
     if (rc == VB_OK && nchunks >= 1) rc = drain(nchunks - 1);

@@ -453,10 +453,32 @@ struct vb_unet {
     // a time per handle
     void* scratch = nullptr;
     size_t scratch_bytes = 0;
+    // per-call work (normalised pairs, padding, tile outputs, percentiles) and
+    // the tile-origin tables of the last geometry, also owned by the handle: a
+    // pageable host->device copy per call would block the host thread until the
+    // stream drains and serialise the stage executor's chunk pipeline
+    void* work = nullptr;
+    size_t work_bytes = 0;
+    int g_h = -1, g_w = -1, g_stride = -1, g_nys = 0, g_nxs = 0;
+    int64_t g_nblk = 0;
+    int2* d_org = nullptr;
+    int* d_pos = nullptr;
 };
 
 namespace vb {
 namespace {
+int grow(void** buf, size_t* have, size_t bytes, cudaStream_t s) {
+    if (bytes > *have) {
+        VB_CUDA(cudaStreamSynchronize(s));  // the old buffer may still be in use by queued work
+        cudaFree(*buf);
+        *buf = nullptr;
+        *have = 0;
+        VB_CUDA(cudaMalloc(buf, bytes));
+        *have = bytes;
+    }
+    return VB_OK;
+}
+
 int net_scratch(vb_unet* net, size_t bytes, cudaStream_t s, void** out) {
     if (bytes > net->scratch_bytes) {
         VB_CUDA(cudaStreamSynchronize(s));  // the old buffer may still be in use by queued work
@@ -678,23 +700,121 @@ int vb_unet_forward(vb_unet* net, const float* patches_dev, int64_t n, float* pr
     return unet_forward(net, a, n, probs_dev, (cudaStream_t)stream);
 }
 
+}  // extern "C"
+
+namespace {
+
+int normalize_impl(const float* sp, const float* tp, int64_t n_blocks, int height, int width, float* out, double* pct,
+                   cudaStream_t s) {
+    const int64_t n = (int64_t)height * width;
+    int rc = percentiles(sp, tp, n, n, n_blocks, pct, s);
+    if (rc) return rc;
+    normalize_kernel<<<grid_for(n_blocks * 2 * n), 256, 0, s>>>(sp, tp, n, n, (int)n_blocks, pct, out);
+    VB_LAUNCHED();
+    return VB_OK;
+}
+
+size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+// tile origins of (h, w, stride) for n_blocks images, cached on the handle
+int tile_tables(vb_unet* net, int ph, int pw, int stride, int64_t n_blocks, cudaStream_t s) {
+    if (net->g_h == ph && net->g_w == pw && net->g_stride == stride && net->g_nblk >= n_blocks) return VB_OK;
+    const std::vector<int> ys = tile_positions(ph, stride), xs = tile_positions(pw, stride);
+    const int tiles = (int)(ys.size() * xs.size());
+    const int64_t nb = std::max<int64_t>(n_blocks, net->g_nblk);
+    std::vector<int2> org((size_t)nb * tiles);
+    for (int64_t b = 0; b < nb; ++b)
+        for (size_t iy = 0; iy < ys.size(); ++iy)
+            for (size_t ix = 0; ix < xs.size(); ++ix) org[(size_t)b * tiles + iy * xs.size() + ix] = make_int2(xs[ix], ys[iy]);
+    std::vector<int> pos(ys);
+    pos.insert(pos.end(), xs.begin(), xs.end());
+    VB_CUDA(cudaStreamSynchronize(s));  // the old tables may still be read by queued work
+    cudaFree(net->d_org);
+    cudaFree(net->d_pos);
+    net->d_org = nullptr;
+    net->d_pos = nullptr;
+    net->g_h = -1;
+    VB_CUDA(cudaMalloc(&net->d_org, org.size() * sizeof(int2)));
+    VB_CUDA(cudaMalloc(&net->d_pos, pos.size() * sizeof(int)));
+    VB_CUDA(cudaMemcpy(net->d_org, org.data(), org.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    VB_CUDA(cudaMemcpy(net->d_pos, pos.data(), pos.size() * sizeof(int), cudaMemcpyHostToDevice));
+    net->g_h = ph;
+    net->g_w = pw;
+    net->g_stride = stride;
+    net->g_nblk = nb;
+    net->g_nys = (int)ys.size();
+    net->g_nxs = (int)xs.size();
+    return VB_OK;
+}
+
+// normalised pairs (device) -> probability maps; `work` holds padding + tile outputs
+int tile_merge_impl(vb_unet* net, const float* normalized, int64_t n_blocks, int height, int width, int stride,
+                    float* prob_dev, char* work, cudaStream_t s) {
+    const int ph = std::max(height, kPatch), pw = std::max(width, kPatch);
+    int rc = tile_tables(net, ph, pw, stride, n_blocks, s);
+    if (rc) return rc;
+    const int tiles = net->g_nys * net->g_nxs;
+    const bool pad = ph != height || pw != width;
+    float* padded = reinterpret_cast<float*>(work);
+    float* probs = reinterpret_cast<float*>(work + (pad ? align256((size_t)n_blocks * 2 * ph * pw * sizeof(float)) : 0));
+    const float* img = normalized;
+    if (pad) {
+        pad_kernel<<<grid_for(n_blocks * 2 * ph * pw), 256, 0, s>>>(normalized, (int)n_blocks * 2, height, width, ph, pw,
+                                                                   padded);
+        VB_LAUNCHED();
+        img = padded;
+    }
+    ConvArgs a;
+    memset(&a, 0, sizeof(a));
+    a.x0 = img;
+    a.mode = 2;
+    a.origins = net->d_org;
+    a.ih = ph;
+    a.iw = pw;
+    a.img_stride = (int64_t)2 * ph * pw;
+    a.tiles_per_img = tiles;
+    rc = unet_forward(net, a, n_blocks * tiles, probs, s);
+    if (rc) return rc;
+    MergeArgs m;
+    m.probs = probs;
+    m.tent = net->tent;
+    m.ys = net->d_pos;
+    m.xs = net->d_pos + net->g_nys;
+    m.nys = net->g_nys;
+    m.nxs = net->g_nxs;
+    m.h = height;
+    m.w = width;
+    m.nblk = (int)n_blocks;
+    m.out = prob_dev;
+    {
+        ProfScope ps(kProfOther, s);
+        merge_kernel<<<grid_for(n_blocks * height * width), 256, 0, s>>>(m);
+    }
+    VB_LAUNCHED();
+    return VB_OK;
+}
+
+size_t tile_merge_work(int64_t n_blocks, int height, int width, int stride) {
+    const int ph = std::max(height, kPatch), pw = std::max(width, kPatch);
+    const size_t tiles = tile_positions(ph, stride).size() * tile_positions(pw, stride).size();
+    const bool pad = ph != height || pw != width;
+    return (pad ? align256((size_t)n_blocks * 2 * ph * pw * sizeof(float)) : 0) +
+           align256((size_t)n_blocks * tiles * kPatch * kPatch * sizeof(float));
+}
+
+}  // namespace
+
+extern "C" {
+
 int vb_normalize_pair(const float* spatial_dev, const float* temporal_dev, int64_t n_blocks, int height, int width,
                       float* out_dev, void* stream) {
     if (!spatial_dev || !temporal_dev || !out_dev) return fail(VB_EINVAL, "null argument");
     if (n_blocks < 1 || height < 1 || width < 1) return fail(VB_EINVAL, "empty summary images");
     cudaStream_t s = (cudaStream_t)stream;
-    const int64_t n = (int64_t)height * width;
     double* pct = nullptr;
     keep_pool();
     VB_CUDA(cudaMallocAsync(&pct, (size_t)n_blocks * 2 * 3 * sizeof(double), s));
-    int rc = percentiles(spatial_dev, temporal_dev, n, n, n_blocks, pct, s);
-    if (rc == VB_OK) {
-        normalize_kernel<<<grid_for(n_blocks * 2 * n), 256, 0, s>>>(spatial_dev, temporal_dev, n, n, (int)n_blocks,
-                                                                     pct, out_dev);
-        launches().fetch_add(1, std::memory_order_relaxed);
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) rc = cuda_fail(e, "normalize_kernel");
-    }
+    const int rc = normalize_impl(spatial_dev, temporal_dev, n_blocks, height, width, out_dev, pct, s);
     cudaFreeAsync(pct, s);
     return rc;
 }
@@ -705,85 +825,28 @@ int vb_unet_tile_merge(vb_unet* net, const float* normalized_dev, int64_t n_bloc
     if (n_blocks < 1 || height < 1 || width < 1) return fail(VB_EINVAL, "empty summary images");
     if (stride < 1) return fail(VB_EINVAL, "stride must be >= 1");
     cudaStream_t s = (cudaStream_t)stream;
-    const int ph = std::max(height, kPatch), pw = std::max(width, kPatch);
-    const std::vector<int> ys = tile_positions(ph, stride), xs = tile_positions(pw, stride);
-    const int tiles = (int)(ys.size() * xs.size());
-    std::vector<int2> org((size_t)n_blocks * tiles);
-    for (int64_t b = 0; b < n_blocks; ++b)
-        for (size_t iy = 0; iy < ys.size(); ++iy)
-            for (size_t ix = 0; ix < xs.size(); ++ix) org[(size_t)b * tiles + iy * xs.size() + ix] = make_int2(xs[ix], ys[iy]);
-    keep_pool();
-    float* padded = nullptr;
-    float* probs = nullptr;
-    int2* d_org = nullptr;
-    int* d_pos = nullptr;
-    const bool pad = ph != height || pw != width;
-    cudaError_t e = cudaSuccess;
-    if (pad) e = cudaMallocAsync(&padded, (size_t)n_blocks * 2 * ph * pw * sizeof(float), s);
-    e = e ? e : cudaMallocAsync(&probs, (size_t)n_blocks * tiles * kPatch * kPatch * sizeof(float), s);
-    e = e ? e : cudaMallocAsync(&d_org, org.size() * sizeof(int2), s);
-    e = e ? e : cudaMallocAsync(&d_pos, (ys.size() + xs.size()) * sizeof(int), s);
-    std::vector<int> pos(ys);
-    pos.insert(pos.end(), xs.begin(), xs.end());
-    e = e ? e : cudaMemcpyAsync(d_org, org.data(), org.size() * sizeof(int2), cudaMemcpyHostToDevice, s);
-    e = e ? e : cudaMemcpyAsync(d_pos, pos.data(), pos.size() * sizeof(int), cudaMemcpyHostToDevice, s);
-    int rc = e == cudaSuccess ? VB_OK : cuda_fail(e, "vb_unet_tile_merge setup");
-    const float* img = normalized_dev;
-    if (rc == VB_OK && pad) {
-        pad_kernel<<<grid_for(n_blocks * 2 * ph * pw), 256, 0, s>>>(normalized_dev, (int)n_blocks * 2, height, width, ph,
-                                                                   pw, padded);
-        launches().fetch_add(1, std::memory_order_relaxed);
-        img = padded;
-    }
-    if (rc == VB_OK) {
-        ConvArgs a;
-        memset(&a, 0, sizeof(a));
-        a.x0 = img;
-        a.mode = 2;
-        a.origins = d_org;
-        a.ih = ph;
-        a.iw = pw;
-        a.img_stride = (int64_t)2 * ph * pw;
-        a.tiles_per_img = tiles;
-        rc = unet_forward(net, a, n_blocks * tiles, probs, s);
-    }
-    if (rc == VB_OK) {
-        MergeArgs m;
-        m.probs = probs;
-        m.tent = net->tent;
-        m.ys = d_pos;
-        m.xs = d_pos + ys.size();
-        m.nys = (int)ys.size();
-        m.nxs = (int)xs.size();
-        m.h = height;
-        m.w = width;
-        m.nblk = (int)n_blocks;
-        m.out = prob_dev;
-        {
-            ProfScope ps(kProfOther, s);
-            merge_kernel<<<grid_for(n_blocks * height * width), 256, 0, s>>>(m);
-        }
-        launches().fetch_add(1, std::memory_order_relaxed);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) rc = cuda_fail(e, "merge_kernel");
-    }
-    if (padded) cudaFreeAsync(padded, s);
-    cudaFreeAsync(probs, s);
-    cudaFreeAsync(d_org, s);
-    cudaFreeAsync(d_pos, s);
-    return rc;
+    int rc = grow(&net->work, &net->work_bytes, tile_merge_work(n_blocks, height, width, stride), s);
+    if (rc) return rc;
+    return tile_merge_impl(net, normalized_dev, n_blocks, height, width, stride, prob_dev,
+                           static_cast<char*>(net->work), s);
 }
 
 int vb_unet_segment(vb_unet* net, const float* spatial_dev, const float* temporal_dev, int64_t n_blocks, int height,
                     int width, int stride, float* normalized_dev, float* prob_dev, void* stream) {
     if (!net || !spatial_dev || !temporal_dev || !prob_dev) return fail(VB_EINVAL, "null argument");
+    if (n_blocks < 1 || height < 1 || width < 1) return fail(VB_EINVAL, "empty summary images");
+    if (stride < 1) return fail(VB_EINVAL, "stride must be >= 1");
     cudaStream_t s = (cudaStream_t)stream;
-    float* norm = normalized_dev;
-    keep_pool();
-    if (!norm) VB_CUDA(cudaMallocAsync(&norm, (size_t)n_blocks * 2 * height * width * sizeof(float), s));
-    int rc = vb_normalize_pair(spatial_dev, temporal_dev, n_blocks, height, width, norm, stream);
-    if (rc == VB_OK) rc = vb_unet_tile_merge(net, norm, n_blocks, height, width, stride, prob_dev, stream);
-    if (!normalized_dev) cudaFreeAsync(norm, s);
+    // work: [pct][normalised pairs (unless the caller keeps them)][tile-merge work]
+    const size_t pct_b = align256((size_t)n_blocks * 6 * sizeof(double));
+    const size_t norm_b = normalized_dev ? 0 : align256((size_t)n_blocks * 2 * height * width * sizeof(float));
+    int rc = grow(&net->work, &net->work_bytes, pct_b + norm_b + tile_merge_work(n_blocks, height, width, stride), s);
+    if (rc) return rc;
+    char* w = static_cast<char*>(net->work);
+    float* norm = normalized_dev ? normalized_dev : reinterpret_cast<float*>(w + pct_b);
+    rc = normalize_impl(spatial_dev, temporal_dev, n_blocks, height, width, norm, reinterpret_cast<double*>(w), s);
+    if (rc == VB_OK)
+        rc = tile_merge_impl(net, norm, n_blocks, height, width, stride, prob_dev, w + pct_b + norm_b, s);
     return rc;
 }
 
@@ -792,6 +855,9 @@ int vb_unet_destroy(vb_unet* net) {
     cudaFree(net->params);
     cudaFree(net->tent);
     cudaFree(net->scratch);
+    cudaFree(net->work);
+    cudaFree(net->d_org);
+    cudaFree(net->d_pos);
     delete net;
     return VB_OK;
 }
