@@ -355,7 +355,10 @@ def run_ours(args):
                           enumerate(["zncc_group", "finalize", "warp_smooth", "median", "other"])}
     hbm_stage = bytes_frame * total_frames / world / (step_ms / 1e3) / 1e9
     roofline = {
-        "bound": "fp32", "kernel": "zncc_group_kernel<21,17>", "plan": pre.plan.info(),
+        "bound": "fp32",
+        "kernel": ("zncc_group_kernel<21,17,1,split>: half-warp per patch, shared middle row" if cfg.radius == 8
+                   else f"zncc_group_kernel<21,{2 * cfg.radius + 1},1>"),
+        "plan": pre.plan.info(),
         "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
         "traffic": traffic,
         "traffic_source": traffic_src,
