@@ -527,6 +527,10 @@ def run_unet(args):
     p2, p1 = _lib.C.c_double(), _lib.C.c_double()
     _lib.check(_lib.load().vb_fp32_peak_probe(_lib.C.byref(p2), _lib.C.byref(p1)))
     peak = max(p2.value, p1.value)
+    # dense TF32 tensor-core peak: half the measured dense BF16 rate (the tcgen05 kind::tf32 rate on B200)
+    peaks, psrc = measured_peaks()
+    tf32_peak = peaks.get("bf16_tflops", 2250.0) / 2.0
+    tf32_src = f"{psrc}: bf16_tflops / 2 (kind::tf32 issues at half the kind::f16 rate)"
     cpu = None
     if not args.no_cpu_baseline:
         try:
@@ -549,9 +553,12 @@ def run_unet(args):
         "vs_baseline": None, "dtype": "f32", "data": "summary pairs of the synthetic C2 recording; random weights",
         "config": {"workload": f"{cfg.name}: {k} blocks of {cfg.height}x{cfg.width}, {tiles} tiles/block, stride 32",
                    "patches_per_step": k * tiles},
-        "roofline": {"bound": "fp32", "achieved": flops / (ms / 1e3) / 1e12, "peak": peak, "unit": "TFLOP/s",
-                     "frac": flops / (ms / 1e3) / 1e12 / peak,
-                     "algorithmic": f"{unet_flops_per_patch():.4g} flop/patch x {k * tiles} patches per step"},
+        "roofline": {"bound": "tensor", "achieved": 3 * flops / (ms / 1e3) / 1e12, "peak": tf32_peak,
+                     "unit": "TFLOP/s", "frac": 3 * flops / (ms / 1e3) / 1e12 / tf32_peak,
+                     "peak_source": tf32_src,
+                     "algorithmic": f"3 x {unet_flops_per_patch():.4g} flop/patch (3xTF32 split on tcgen05) x "
+                                    f"{k * tiles} patches per step",
+                     "fp32_equivalent": {"achieved": flops / (ms / 1e3) / 1e12, "peak_fp32_simt": peak}},
         "cpu_baseline": cpu, "gpu_launches": int(launches), "clocks": clk,
     }
     print(json.dumps(line), flush=True)
