@@ -199,14 +199,27 @@ __device__ __forceinline__ void box_ready(const ZnccArgs& a, uint64_t* bar, uint
 // sums down all S rows (a single round for groups up to 256 columns wide),
 // then one thread per (patch, dy) row slides horizontally.  The next frame's
 // box is fetched while this frame's horizontal pass runs.
-template <bool INT, int P_CT>
+#ifndef VB_FAST_RSQRT
+#define VB_FAST_RSQRT 0  // measured: the MUFU seed + Newton step was slower (2.06 vs 1.99 ms per 4000 C2 frames)
+#endif
+constexpr bool kFastRsqrt = VB_FAST_RSQRT;
+// 1/sqrt(x) for positive normal x: f32 MUFU seed + one float64 Newton step
+// (relative error ~2^-46; the result is rounded to f32 anyway), branch-free
+// unlike the library's double rsqrt.  Falls back when x leaves the f32 range.
+__device__ __forceinline__ double rsqrt_pos(double x) {
+    if (x < 1e-30 || x > 1e30) return rsqrt(x);
+    const double y = (double)rsqrtf((float)x);
+    return y * fma(-0.5 * x * y, y, 1.5);
+}
+
+template <bool INT, int P_CT, int S_CT = 0>
 __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __grid_constant__ CUtensorMap tmap) {
     using T1 = typename std::conditional<INT, int, double>::type;        // sample / sum of f
     using T2 = typename std::conditional<INT, long long, double>::type;  // sum of f^2
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar;
     const int P = P_CT ? P_CT : a.P;  // compile-time patch: fully unrolled window sums
-    const int S = a.S, SS = S * S;
+    const int S = S_CT ? S_CT : a.S, SS = S * S;
     const PatchGroup grp = a.groups[blockIdx.x];
     const int G = grp.count, wu = grp.wu, vp = wu | 1;
     const double nn = (double)P * (double)P;
@@ -272,7 +285,9 @@ __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __gri
                 h2 += r2[xx];
             }
             float* out = a.inv + ((size_t)t * a.n_patches + gp) * SS + (size_t)dy * S;
-            for (int dx = 0; dx < S; ++dx) {
+#pragma unroll
+            for (int dx = 0; dx < (S_CT ? S_CT : 64); ++dx) {
+                if (!S_CT && dx >= S) break;
                 float iv = 0.0f;
                 if constexpr (INT) {
                     // n*fvar exactly; 1/sqrt(fvar*rv) = P / sqrt(n*fvar*rv).  int64 -> f64 by
@@ -280,7 +295,7 @@ __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __gri
                     const long long nf = (long long)P * P * h2 - (long long)h1 * h1;
                     if (rv > 0.0 && nf > 0) {
                         const double nfd = __longlong_as_double(0x4330000000000000LL | nf) - 4503599627370496.0;
-                        iv = (float)((double)P * rsqrt(nfd * rv));
+                        iv = (float)((double)P * (kFastRsqrt ? rsqrt_pos(nfd * rv) : rsqrt(nfd * rv)));
                     }
                 } else {
                     const double fvar = h2 - h1 * h1 / nn;  // kernels.py:67
@@ -797,6 +812,13 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     void (*stats_fn)(ZnccArgs, CUtensorMap) =
         patch == 21 ? (dtype == VB_U16 ? zncc_stats_kernel<true, 21> : zncc_stats_kernel<false, 21>)
                     : (dtype == VB_U16 ? zncc_stats_kernel<true, 0> : zncc_stats_kernel<false, 0>);
+    static const bool no_stats_s = getenv("VB_NO_STATS_S") != nullptr;  // experiment knob
+    if (patch == 21 && dtype == VB_U16 && !no_stats_s) {  // compile-time S: unrolled horizontal chains
+        if (S == 17) stats_fn = zncc_stats_kernel<true, 21, 17>;
+        if (S == 21) stats_fn = zncc_stats_kernel<true, 21, 21>;
+        if (S == 25) stats_fn = zncc_stats_kernel<true, 21, 25>;
+        if (S == 11) stats_fn = zncc_stats_kernel<true, 21, 11>;
+    }
     SmemPlan sp = zncc_smem(patch, radius, t.max_g, t.max_wu, dtype, fpi, fast, t.pitch);
     if (std::max(sp.total, sp.stats_total) > 227 * 1024)
         return fail(VB_EINVAL, "patch group does not fit in shared memory");
