@@ -483,6 +483,9 @@ __global__ void __launch_bounds__(kK3Threads, 3) warp_smooth_tma_kernel(K3Args a
 //  C  horizontal pass: 8 outputs per thread from 26 samples, float4 stores.
 // The next frame's box is issued right after A1 (raw box consumed).
 constexpr int kVR2 = 11;  // vertical-pass outputs per thread: kTY = 11 + 11 + 10
+#ifndef VB_K3_INTERLEAVE
+#define VB_K3_INTERLEAVE 1
+#endif
 #ifndef VB_K3V2_MIN_BLOCKS
 #define VB_K3V2_MIN_BLOCKS 3  // measured: 80 regs x 3 CTAs beats a 64-reg cap (spills) x 4
 #endif
@@ -628,6 +631,23 @@ __global__ void __launch_bounds__(kK3Threads, kK3V2MinBlocks) warp_smooth_v2_ker
             double x[kVR2 + 2 * WR];
 #pragma unroll
             for (int q = 0; q < kVR2 + 2 * WR; ++q) x[q] = (r0 + q < EH) ? (double)sC[(r0 + q) * EWP + c] : 0.0;
+#if VB_K3_INTERLEAVE
+            // all outputs advance together tap by tap: kVR2 independent chains
+            // per step (same per-output operation order); weights from the
+            // kernel-parameter constant bank (w symmetric: w[-k] == w[+k])
+            double acc[kVR2];
+#pragma unroll
+            for (int j = 0; j < kVR2; ++j) acc[j] = __dmul_rn(x[j + WR], a.wt.w[WR]);
+#pragma unroll
+            for (int k = WR; k >= 1; --k) {
+#pragma unroll
+                for (int j = 0; j < kVR2; ++j)
+                    acc[j] = __dadd_rn(acc[j], __dmul_rn(__dadd_rn(x[j + WR - k], x[j + WR + k]), a.wt.w[WR - k]));
+            }
+#pragma unroll
+            for (int j = 0; j < kVR2; ++j)
+                if (j < nout) sV[(r0 + j) * EWP + c] = (float)acc[j];
+#else
 #pragma unroll
             for (int j = 0; j < kVR2; ++j) {
                 if (j < nout) {
@@ -638,6 +658,7 @@ __global__ void __launch_bounds__(kK3Threads, kK3V2MinBlocks) warp_smooth_v2_ker
                     sV[(r0 + j) * EWP + c] = (float)acc;
                 }
             }
+#endif
         }
         __syncthreads();
         // C: horizontal pass -> smoothed frame.  Lanes take consecutive rows.
@@ -648,6 +669,19 @@ __global__ void __launch_bounds__(kK3Threads, kK3V2MinBlocks) warp_smooth_v2_ker
 #pragma unroll
             for (int q = 0; q < HR + 2 * WR; ++q) x[q] = (double)sV[ly * EWP + lx0 + q];
             float o[HR];
+#if VB_K3_INTERLEAVE
+            double acc[HR];
+#pragma unroll
+            for (int j = 0; j < HR; ++j) acc[j] = __dmul_rn(x[j + WR], a.wt.w[WR]);
+#pragma unroll
+            for (int k = WR; k >= 1; --k) {
+#pragma unroll
+                for (int j = 0; j < HR; ++j)
+                    acc[j] = __dadd_rn(acc[j], __dmul_rn(__dadd_rn(x[j + WR - k], x[j + WR + k]), a.wt.w[WR - k]));
+            }
+#pragma unroll
+            for (int j = 0; j < HR; ++j) o[j] = (float)acc[j];
+#else
 #pragma unroll
             for (int j = 0; j < HR; ++j) {
                 double acc = __dmul_rn(x[j + WR], wk[0]);
@@ -655,6 +689,7 @@ __global__ void __launch_bounds__(kK3Threads, kK3V2MinBlocks) warp_smooth_v2_ker
                 for (int k = WR; k >= 1; --k) acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(x[j + WR - k], x[j + WR + k]), wk[k]));
                 o[j] = (float)acc;
             }
+#endif
             const int gy = ty0 + ly, gx0 = tx0 + lx0;
             float* dst = a.smoothed + t * hw + (int64_t)gy * a.w + gx0;
             if (gy < a.h) {
