@@ -357,6 +357,10 @@ __device__ __forceinline__ void cross_row(const float* __restrict__ reg, int pit
 // d in {4, 13..16} add template rows {8, 17..20} -- so every window sample
 // loaded for the lane's own row serves the shared row too.  The half-warp
 // then sums the shared row's partials in a fixed shuffle tree.
+#ifndef VB_SPLIT_UNROLL
+#define VB_SPLIT_UNROLL 1  // measured: 3 -> 7.41 ms, 7 -> 9.16 ms (instruction cache) vs 7.12 ms
+#endif
+constexpr int kSplitUnroll = VB_SPLIT_UNROLL;
 #ifndef VB_SPLIT_PREFETCH
 #define VB_SPLIT_PREFETCH 4  // measured: 7.57 -> 7.29 ms per 4000 C2 frames (4 or 8 samples alike)
 #endif
@@ -391,7 +395,7 @@ __device__ __forceinline__ void cross_row_split17(const float* __restrict__ reg,
 #pragma unroll
     for (int i = 0; i < PF; ++i) w_next[i] = reg[i];
 #endif
-#pragma unroll 1
+#pragma unroll kSplitUnroll
     for (int yy = 0; yy < P; ++yy) {
         const float* fr = reg + yy * pitch;
         float win[S + P - 1];
