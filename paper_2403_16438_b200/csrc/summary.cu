@@ -943,9 +943,36 @@ __global__ void __launch_bounds__(kK4Threads) median_kernel(K4Args a) {
     const int rows = cnt + 2 * hh;
     const int64_t p0 = (int64_t)blockIdx.x * kK4Pix;
     const int np = (int)((int64_t)kK4Pix < a.hw - p0 ? (int64_t)kK4Pix : a.hw - p0);
-    // staging: 16 independent loads in flight per thread before their stores
-    // (the phase is latency-bound; each warp row is 2 x 64 contiguous bytes)
-    {
+    // staging: float4 loads (4 pixels of one frame row; 4 threads per 64-byte
+    // row segment), 8 independent loads in flight per thread before their
+    // stores; the scalar path covers frames whose rows are not 16-byte aligned
+    if ((a.hw & 3) == 0 && np == kK4Pix) {
+        constexpr int kB = 8;
+        const int total4 = rows * (kK4Pix / 4);
+        for (int i0 = threadIdx.x; i0 < total4; i0 += kB * kK4Threads) {
+            float4 vals[kB];
+#pragma unroll
+            for (int j = 0; j < kB; ++j) {
+                const int i = i0 + j * kK4Threads;
+                const int tt = i >> 2, q = i & 3;
+                int64_t g = t0 - hh + tt;
+                if constexpr (HP) g = reflect64(g, a.t_total);
+                vals[j] = i < total4 ? __ldcs(reinterpret_cast<const float4*>(a.sm + (g - a.s_lo) * a.hw + p0) + q)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int j = 0; j < kB; ++j) {
+                const int i = i0 + j * kK4Threads;
+                if (i < total4) {
+                    float* d = sm4 + (i >> 2) * ST + (i & 3) * 4;
+                    d[0] = vals[j].x;
+                    d[1] = vals[j].y;
+                    d[2] = vals[j].z;
+                    d[3] = vals[j].w;
+                }
+            }
+        }
+    } else {
         constexpr int kB = 16;
         const int total = rows * kK4Pix;
         for (int i0 = threadIdx.x; i0 < total; i0 += kB * kK4Threads) {
