@@ -52,6 +52,11 @@ struct vb_stage {
     float* d_gain = nullptr;
     int64_t cap = 0;  // frames per ring slot (chunk + high-pass halo)
     cudaEvent_t ev_h2d[2]{}, ev_comp[2]{}, ev_d2h[2]{};
+    // a chunk is uploaded in kSubParts pieces, each with its own event, so the
+    // motion search of a chunk's first frames starts while the rest is still
+    // crossing PCIe (shorter pipeline fill and drain around the H2D-bound body)
+    static constexpr int kSubParts = 4;
+    cudaEvent_t ev_sub[2][kSubParts]{};
     int64_t last_launches = 0;
     // SURVEY 8(f) rows 2 + 4: per-block U-Net segmentation of each chunk's
     // summaries on its own stream (overlapping the next chunk's motion search),
@@ -134,6 +139,8 @@ int vb_stage_create(vb_stage** out, const vb_stage_config* cfg) {
     e = e ? e : cudaStreamCreateWithFlags(&st->s_d2h, cudaStreamNonBlocking);
     for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
         e = cudaEventCreateWithFlags(&st->ev_h2d[i], cudaEventDisableTiming);
+        for (int j = 0; j < vb_stage::kSubParts && e == cudaSuccess; ++j)
+            e = cudaEventCreateWithFlags(&st->ev_sub[i][j], cudaEventDisableTiming);
         e = e ? e : cudaEventCreateWithFlags(&st->ev_comp[i], cudaEventDisableTiming);
         e = e ? e : cudaEventCreateWithFlags(&st->ev_d2h[i], cudaEventDisableTiming);
     }
@@ -290,18 +297,24 @@ static int stage_run(vb_stage* st, const void* frames_host, int dtype, int64_t n
         return std::make_pair(std::max<int64_t>(0, f0 - hh), std::min<int64_t>(n_frames, f0 + nf + hh));
     };
 
-    // host->device copy of frames [f0, f0+nf) into slot
+    // the kSubParts pieces of an nf-frame slot load: piece j = [part(j), part(j+1))
+    auto nparts = [&](int64_t nf) { return (int)std::min<int64_t>(vb_stage::kSubParts, std::max<int64_t>(1, nf)); };
+    auto part = [&](int64_t nf, int j) { return nf * j / nparts(nf); };
+    // host->device copy of frames [f0, f0+nf) into slot, piece by piece
     auto upload = [&](int slot, int64_t f0, int64_t nf) -> int {
-        const char* src = (const char*)frames_host + (size_t)f0 * hw * esz;
-        const size_t bytes = (size_t)nf * hw * esz;
-        if (!pinned) {
-            // staging slot is free once its previous upload completed
-            VB_CUDA(cudaEventSynchronize(st->ev_h2d[slot]));
-            memcpy(st->h_stage[slot], src, bytes);
-            src = (const char*)st->h_stage[slot];
-        }
+        if (!pinned) VB_CUDA(cudaEventSynchronize(st->ev_h2d[slot]));  // staging slot free again
         VB_CUDA(cudaStreamWaitEvent(st->s_h2d, st->ev_comp[slot], 0));  // slot no longer read by compute
-        VB_CUDA(cudaMemcpyAsync(st->d_frames[slot], src, bytes, cudaMemcpyHostToDevice, st->s_h2d));
+        for (int j = 0; j < nparts(nf); ++j) {
+            const int64_t p0 = part(nf, j), p1 = part(nf, j + 1);
+            const size_t off = (size_t)p0 * hw * esz, bytes = (size_t)(p1 - p0) * hw * esz;
+            const char* src = (const char*)frames_host + (size_t)f0 * hw * esz + off;
+            if (!pinned) {
+                memcpy((char*)st->h_stage[slot] + off, src, bytes);
+                src = (const char*)st->h_stage[slot] + off;
+            }
+            VB_CUDA(cudaMemcpyAsync((char*)st->d_frames[slot] + off, src, bytes, cudaMemcpyHostToDevice, st->s_h2d));
+            VB_CUDA(cudaEventRecord(st->ev_sub[slot][j], st->s_h2d));
+        }
         VB_CUDA(cudaEventRecord(st->ev_h2d[slot], st->s_h2d));
         return VB_OK;
     };
@@ -320,9 +333,11 @@ static int stage_run(vb_stage* st, const void* frames_host, int dtype, int64_t n
     const bool chunk0_resident = m > 0 && m <= C;
     int rc = VB_OK;
     if (chunk0_resident) {
-        rc = upload(0, 0, avail(0, std::min<int64_t>(C, n_frames)).second);
-        if (rc == VB_OK) {
-            VB_CUDA(cudaStreamWaitEvent(st->s_comp, st->ev_h2d[0], 0));
+        const int64_t n0 = avail(0, std::min<int64_t>(C, n_frames)).second;
+        rc = upload(0, 0, n0);
+        if (rc == VB_OK) {  // only the pieces holding the first m frames
+            for (int j = 0; j < nparts(n0) && part(n0, j) < m; ++j)
+                VB_CUDA(cudaStreamWaitEvent(st->s_comp, st->ev_sub[0][j], 0));
             rc = launch_template_sum(st->d_frames[0], dtype, m, (int64_t)hw, st->d_tsum, 0, st->s_comp);
         }
     } else {
@@ -367,10 +382,13 @@ static int stage_run(vb_stage* st, const void* frames_host, int dtype, int64_t n
         const auto [a0, a1] = avail(f0, nf);
         if (k == 0 && !chunk0_resident) rc = upload(slot, a0, a1 - a0);  // later chunks are prefetched below
         if (rc) break;
-        VB_CUDA(cudaStreamWaitEvent(st->s_comp, st->ev_h2d[slot], 0));
         VB_CUDA(cudaStreamWaitEvent(st->s_comp, st->ev_d2h[slot], 0));  // outputs of chunk k-2 drained
-        rc = vb_motion_estimate(st->plan, st->d_frames[slot], dtype, a1 - a0, c.subpixel, st->d_vec[slot], nullptr,
-                                st->s_comp);
+        for (int j = 0; j < nparts(a1 - a0) && rc == VB_OK; ++j) {  // search each piece as it lands
+            const int64_t p0 = part(a1 - a0, j), p1 = part(a1 - a0, j + 1);
+            VB_CUDA(cudaStreamWaitEvent(st->s_comp, st->ev_sub[slot][j], 0));
+            rc = vb_motion_estimate(st->plan, (const char*)st->d_frames[slot] + (size_t)p0 * hw * esz, dtype, p1 - p0,
+                                    c.subpixel, st->d_vec[slot] + p0, nullptr, st->s_comp);
+        }
         if (rc) break;
         float* corr = corrected_dev ? corrected_dev + (size_t)f0 * hw : (corrected_host ? st->d_corr[slot] : nullptr);
         SummaryOpts so;
@@ -440,6 +458,8 @@ int vb_stage_destroy(vb_stage* st) {
     cudaFree(st->d_gain);
     for (int i = 0; i < 2; ++i) {
         if (st->ev_h2d[i]) cudaEventDestroy(st->ev_h2d[i]);
+        for (int j = 0; j < vb_stage::kSubParts; ++j)
+            if (st->ev_sub[i][j]) cudaEventDestroy(st->ev_sub[i][j]);
         if (st->ev_comp[i]) cudaEventDestroy(st->ev_comp[i]);
         if (st->ev_d2h[i]) cudaEventDestroy(st->ev_d2h[i]);
     }
