@@ -190,6 +190,22 @@ int vb_block_finish(const float* smoothed_dev, int64_t s_lo, int64_t n_smoothed,
                     int64_t t_total, int highpass_window, int height, int width, const double* sum_dev,
                     float* spatial_dev, float* temporal_dev, void* stream);
 
+/* Peer memory for the exchange of straddling blocks between ranks (SURVEY
+ * 8(e)): the receiving rank allocates its block buffers with vb_ipc_alloc and
+ * shares the 64-byte handle; the sending rank opens it (vb_ipc_open, peer
+ * access over NVLink when the ranks are on different GPUs) and passes the
+ * mapped pointers to vb_block_piece, so the warp+smooth kernel and the running
+ * sum write the block straight into the owner's memory, tile by tile, with no
+ * separate copy.  vb_copy_async (cudaMemcpyDefault) relays a received prefix
+ * to the next owner; vb_memset_async zeroes a (peer) running sum. */
+#define VB_IPC_HANDLE_BYTES 64
+int vb_ipc_alloc(int64_t bytes, void** dev_ptr, unsigned char* handle);
+int vb_ipc_open(const unsigned char* handle, void** dev_ptr);
+int vb_ipc_close(void* dev_ptr);
+int vb_ipc_free(void* dev_ptr);
+int vb_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+int vb_memset_async(void* dst, int value, int64_t bytes, void* stream);
+
 /* ---------------- summary normalisation + U-Net tiles ----------------
  * The consumer of the per-block summaries in the reference pipeline
  * (pipeline.py:222-223).  Parameters are the float32 tensors of

@@ -56,5 +56,10 @@ def motion_to_numpy(buf: torch.Tensor, n: int) -> np.ndarray:
     return raw.view(_lib.MOTION_DTYPE).copy()
 
 
-def ptr(t: torch.Tensor | None) -> int | None:
-    return None if t is None else t.data_ptr()
+def ptr(t) -> int | None:
+    """Device address of a tensor; raw integer addresses (IPC-mapped peer
+    memory, which torch must not wrap -- it would copy it to the local device)
+    pass through."""
+    if t is None:
+        return None
+    return int(t) if isinstance(t, int) else t.data_ptr()

@@ -65,6 +65,12 @@ SIGNATURES = {
                                _vp, _vp, _vp, _vp]),
     "vb_block_piece": (_i32, [_vp, _i32, _vp, _i64, _i32, _i32, _vp, _i32, _vp, _i64, _i64, _vp, _vp, _vp, _vp]),
     "vb_block_finish": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "vb_ipc_alloc": (_i32, [_i64, C.POINTER(_vp), _vp]),
+    "vb_ipc_open": (_i32, [_vp, C.POINTER(_vp)]),
+    "vb_ipc_close": (_i32, [_vp]),
+    "vb_ipc_free": (_i32, [_vp]),
+    "vb_copy_async": (_i32, [_vp, _vp, _i64, _vp]),
+    "vb_memset_async": (_i32, [_vp, _i32, _i64, _vp]),
     "vb_unet_param_count": (_i64, []),
     "vb_unet_create": (_i32, [C.POINTER(_vp), _vp, _i64]),
     "vb_unet_forward": (_i32, [_vp, _vp, _i64, _vp, _vp]),

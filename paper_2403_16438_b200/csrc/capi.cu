@@ -252,6 +252,53 @@ const char* vb_version(void) { return "voltb200 0.1 (sm_100a)"; }
 const char* vb_last_error(void) { return g_err.c_str(); }
 int64_t vb_launch_count(void) { return g_launches.load(); }
 
+// ---- peer memory for the frame-balanced shards' block exchange ----
+int vb_ipc_alloc(int64_t bytes, void** dev_ptr, unsigned char* handle) {
+    if (!dev_ptr || !handle || bytes <= 0) return fail(VB_EINVAL, "null argument");
+    *dev_ptr = nullptr;
+    VB_CUDA(cudaMalloc(dev_ptr, (size_t)bytes));
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, *dev_ptr);
+    if (e != cudaSuccess) {
+        cudaFree(*dev_ptr);
+        *dev_ptr = nullptr;
+        return cuda_fail(e, "cudaIpcGetMemHandle");
+    }
+    static_assert(sizeof(cudaIpcMemHandle_t) == VB_IPC_HANDLE_BYTES, "IPC handle size");
+    memcpy(handle, &h, sizeof(h));
+    return VB_OK;
+}
+
+int vb_ipc_open(const unsigned char* handle, void** dev_ptr) {
+    if (!handle || !dev_ptr) return fail(VB_EINVAL, "null argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    VB_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return VB_OK;
+}
+
+int vb_ipc_close(void* dev_ptr) {
+    if (dev_ptr) VB_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+    return VB_OK;
+}
+
+int vb_ipc_free(void* dev_ptr) {
+    if (dev_ptr) VB_CUDA(cudaFree(dev_ptr));
+    return VB_OK;
+}
+
+int vb_memset_async(void* dst, int value, int64_t bytes, void* stream) {
+    if (!dst && bytes > 0) return fail(VB_EINVAL, "null argument");
+    if (bytes > 0) VB_CUDA(cudaMemsetAsync(dst, value, (size_t)bytes, (cudaStream_t)stream));
+    return VB_OK;
+}
+
+int vb_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+    if ((!dst || !src) && bytes > 0) return fail(VB_EINVAL, "null argument");
+    if (bytes > 0) VB_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, (cudaStream_t)stream));
+    return VB_OK;
+}
+
 int vb_patch_grid(int height, int width, int patch, int margin, int32_t* origins, int* n_origins) {
     const int lo_x = margin, hi_x = width - margin - patch;
     const int lo_y = margin, hi_y = height - margin - patch;

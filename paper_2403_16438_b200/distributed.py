@@ -349,7 +349,7 @@ class DeviceOps:
         pre = self.pre
         _lib.call("vb_block_piece", frames.data_ptr(), D.vb_dtype(frames), D.ptr(vec), n, h, w,
                   pre.weights.ctypes.data, pre.wradius, D.ptr(pre.gain), mean_off, mean_n, D.ptr(corrected_out),
-                  smoothed.data_ptr(), partial.data_ptr(), D.stream_handle())
+                  D.ptr(smoothed), D.ptr(partial), D.stream_handle())
 
     def finish(self, smoothed, s_lo, t0, count, t_total, partial):
         from . import _device as D
@@ -377,6 +377,106 @@ class ShardResult:
         return D.motion_to_numpy(self.vectors, self.n_frames)
 
 
+class _CudaArray:
+    """Zero-copy torch view of a raw device allocation (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, shape: tuple, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def _wrap(ptr: int, shape: tuple, dtype) -> torch.Tensor:
+    typestr = {torch.float32: "<f4", torch.float64: "<f8"}[dtype]
+    return torch.as_tensor(_CudaArray(ptr, shape, typestr), device="cuda")
+
+
+class _Tokens:
+    """Ordering messages between neighbour ranks for the peer-memory exchange:
+    READY (the block data has been written into the owner's memory) and ACK
+    (the owner has consumed its buffers; the sender may overwrite them next
+    run).  NCCL tokens are stream-ordered; gloo tokens (CPU tests, ranks
+    sharing one GPU) follow a stream synchronisation."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.nccl = dist.get_backend(group) == "nccl"
+        self._keep = []
+
+    def send(self, peer: int) -> None:
+        """Never waited on inside a run: an ACK is only received by the peer's
+        next run, after the next collective (waiting here would deadlock it)."""
+        if self.nccl:
+            t = torch.ones(1, device="cuda")
+        else:
+            torch.cuda.current_stream().synchronize()
+            t = torch.ones(1)
+        self._keep = [(x, w) for x, w in self._keep if not w.is_completed()]
+        self._keep.append((t, dist.isend(t, peer, self.group)))
+
+    def recv(self, peer: int) -> None:
+        t = torch.empty(1, device="cuda") if self.nccl else torch.empty(1)
+        dist.irecv(t, peer, self.group).wait()
+
+    def drain(self) -> None:
+        for _t, w in self._keep:
+            w.wait()
+        self._keep.clear()
+
+
+class _PeerBlocks:
+    """IPC buffers of the straddling-block exchange: each rank
+    that finishes or relays a block allocates its receive buffers with
+    vb_ipc_alloc; the sender maps its next owner's buffers (vb_ipc_open) and
+    its warp+smooth kernel and running sum write the block there directly
+    (over NVLink on a multi-GPU node), tile by tile, instead of a separate
+    send of the finished buffers."""
+
+    def __init__(self, shard: BalancedShard, height: int, width: int, group=None):
+        from . import _lib
+
+        self.lib = _lib
+        hw = height * width
+        self.own = None    # (buf ptr, sum ptr) of this rank's head piece
+        self.peer = None   # (buf ptr, sum ptr) mapped from the next owner
+        self._alloc = []
+        mine = {}
+        if shard.head is not None:
+            p = shard.head
+            nbuf = (p.c_hi - p.s_lo) * hw * 4
+            bptr, bh = self._ipc_alloc(nbuf)
+            sptr, sh = self._ipc_alloc(hw * 8)
+            self.own = (bptr, sptr)
+            mine = {"buf": bh, "sum": sh}
+        handles = [None] * shard.world
+        dist.all_gather_object(handles, mine, group)
+        nxt = shard.tail.next if shard.tail is not None else (
+            shard.head.next if shard.head is not None and shard.head.role == "middle" else None)
+        if nxt is not None:
+            self.peer = (self._ipc_open(handles[nxt]["buf"]), self._ipc_open(handles[nxt]["sum"]))
+
+    def _ipc_alloc(self, nbytes: int):
+        import ctypes as C
+        ptr = C.c_void_p()
+        handle = (C.c_ubyte * 64)()
+        self.lib.call("vb_ipc_alloc", nbytes, C.byref(ptr), handle)
+        self._alloc.append(("free", ptr.value))
+        return ptr.value, bytes(handle)
+
+    def _ipc_open(self, handle: bytes) -> int:
+        import ctypes as C
+        ptr = C.c_void_p()
+        buf = (C.c_ubyte * 64).from_buffer_copy(handle)
+        self.lib.call("vb_ipc_open", buf, C.byref(ptr))
+        self._alloc.append(("close", ptr.value))
+        return ptr.value
+
+    def close(self) -> None:
+        lib = self.lib.load()
+        for kind, ptr in reversed(self._alloc):
+            (lib.vb_ipc_close if kind == "close" else lib.vb_ipc_free)(ptr)
+        self._alloc.clear()
+
+
 class BalancedShardedPreprocessor:
     """Per-rank driver over frame-balanced shards (balanced_plan):
     template all-reduce -> motion search of every local frame -> the tail
@@ -385,14 +485,25 @@ class BalancedShardedPreprocessor:
     block's last frame) finished.  `ops` defaults to the CUDA entry points;
     the CPU tests pass an oracle-backed stand-in to check the protocol."""
 
-    def __init__(self, height: int, width: int, config=None, group=None, ops=None):
+    def __init__(self, height: int, width: int, config=None, group=None, ops=None, exchange: str = "peer"):
+        """exchange: "peer" -- the sender's kernels write the straddling block
+        straight into the owner's IPC-mapped buffers (device ops only); "p2p" --
+        the finished buffers are sent with NCCL / gloo point-to-point."""
         if ops is None:
             from . import stage
 
             ops = DeviceOps(stage.DevicePreprocessor(height, width, config))
+        if exchange not in ("peer", "p2p"):
+            raise ValueError("exchange must be 'peer' or 'p2p'")
         self.ops = ops
         self.group = group
         self.height, self.width = height, width
+        self.exchange = exchange if isinstance(ops, DeviceOps) else "p2p"
+        self._peer = None
+        self._peer_key = None
+        self._tokens = None
+        self._runs = 0
+        self._tail_next = None
 
     def run(self, frames_local, shard: BalancedShard, ref_frames: int, corrected_out=None) -> ShardResult:
         """frames_local = recording frames [shard.local_lo, shard.local_hi);
@@ -412,6 +523,8 @@ class BalancedShardedPreprocessor:
             ops.piece(frames_local[p.c_lo - base:p.c_hi - base], ops.vec_slice(vec, p.c_lo - base, p.c_hi - base),
                       p.m_lo - p.c_lo, p.m_hi - p.m_lo, corr(p.m_lo, p.m_hi), smoothed, acc)
 
+        if s.world > 1 and self.exchange == "peer":
+            return self._run_peer(frames_local, s, vec, corr, run_piece, corrected_out)
         p2p = _P2P(self.group) if s.world > 1 else None
         sends, recvs = [], []
         if s.tail is not None:  # this rank starts a block that a later rank finishes
@@ -454,7 +567,81 @@ class BalancedShardedPreprocessor:
         assert sp.shape[0] == s.block_hi - s.block_lo
         return ShardResult(vec, sp, tp, corrected_out, frames_local.shape[0])
 
+    def _run_peer(self, frames_local, s: BalancedShard, vec, corr, run_piece, corrected_out) -> ShardResult:
+        """The straddling-block exchange through peer memory (see _PeerBlocks)."""
+        ops, base, T = self.ops, s.local_lo, s.n_total
+        h, w = self.height, self.width
+        key = (s.rank, s.world, s.frame_lo, s.frame_hi, s.local_lo, s.local_hi, s.n_total)
+        if self._peer_key != key:  # collective: every rank (re)maps together
+            if self._peer is not None:
+                self._peer.close()
+            self._peer = _PeerBlocks(s, h, w, self.group)
+            self._peer_key = key
+            self._tokens = _Tokens(self.group)
+            self._runs = 0
+        pb, tk = self._peer, self._tokens
+        first = self._runs == 0
+        self._tail_next = s.tail.next if s.tail is not None else (
+            s.head.next if s.head is not None and s.head.role == "middle" else None)
+        if s.tail is not None:  # write this rank's piece into the next owner's buffers
+            p = s.tail
+            if not first:
+                tk.recv(p.next)  # ACK: the owner is done with last run's data
+            from . import _device as D
+            from . import _lib
+            _lib.call("vb_memset_async", pb.peer[1], 0, h * w * 8, D.stream_handle())  # the sum starts at 0
+            run_piece(p, pb.peer[0], pb.peer[1])  # raw peer addresses: the kernels write the owner's memory
+            tk.send(p.next)  # READY
+        whole = None
+        if s.whole_hi > s.whole_lo:
+            whole = ops.whole(frames_local, vec, base, T, (s.whole_lo - base, s.whole_hi - s.whole_lo),
+                              corr(s.whole_lo, s.whole_hi))
+        sp_parts, tp_parts = [], []
+        if s.head is not None:
+            p = s.head
+            n_buf = p.c_hi - p.s_lo
+            head_buf = _wrap(pb.own[0], (n_buf, h, w), torch.float32)
+            head_sum = _wrap(pb.own[1], (h, w), torch.float64)
+            tk.recv(p.prev)  # READY: the earlier contributors' frames and running sum are in place
+            if p.role == "middle":  # relay: prefix and sum to the next owner, own piece written there directly
+                if not first:
+                    tk.recv(p.next)
+                nb, ns = pb.peer
+                from . import _device as D
+                from . import _lib
+                npre = p.c_lo - p.s_lo
+                _lib.call("vb_copy_async", nb, head_buf.data_ptr(), npre * h * w * 4, D.stream_handle())
+                _lib.call("vb_copy_async", ns, head_sum.data_ptr(), h * w * 8, D.stream_handle())
+                run_piece(p, nb + npre * h * w * 4, ns)
+                tk.send(p.next)
+            else:
+                run_piece(p, head_buf[p.c_lo - p.s_lo:], head_sum)
+                sp_h, tp_h = ops.finish(head_buf, p.s_lo, p.t0, p.t1 - p.t0, T, head_sum)
+                sp_parts.append(sp_h)
+                tp_parts.append(tp_h)
+            tk.send(p.prev)  # ACK for the next run (stream-ordered after the reads above)
+        if whole is not None:
+            sp_parts.append(whole[0])
+            tp_parts.append(whole[1])
+        if sp_parts:
+            sp, tp = torch.cat(sp_parts), torch.cat(tp_parts)
+        else:
+            sp = torch.empty((0, h, w), dtype=torch.float32, device=frames_local.device)
+            tp = sp.clone()
+        self._runs += 1
+        assert sp.shape[0] == s.block_hi - s.block_lo
+        return ShardResult(vec, sp, tp, corrected_out, frames_local.shape[0])
+
     def close(self):
+        """Collective with the neighbours: outstanding ACKs are matched first."""
+        if self._peer is not None:
+            torch.cuda.synchronize()
+            s_tail = self._peer_key is not None and self._runs > 0
+            if s_tail and self._tail_next is not None:
+                self._tokens.recv(self._tail_next)  # the last run's ACK
+            self._tokens.drain()
+            self._peer.close()
+            self._peer = None
         close = getattr(getattr(self.ops, "pre", None), "close", None)
         if close is not None:
             close()

@@ -1,10 +1,12 @@
 """Frame-balanced time shards on the CUDA path: W ranks (gloo,
-all on cuda:0 -- every exchange is host-mediated, no kernel waits on another
-rank) run BalancedShardedPreprocessor with the C-ABI entry points
-vb_block_piece / vb_block_finish for the blocks that straddle ranks; the
-gathered outputs must equal the single-device run bit for bit (vectors,
-corrected frames, spatial and temporal summaries), with and without the A17
-options."""
+all on cuda:0 -- every ordering token is host-mediated, no kernel waits on
+another rank) run BalancedShardedPreprocessor with the C-ABI entry points
+vb_block_piece / vb_block_finish for the blocks that straddle ranks, both
+with the peer-memory exchange (the sender's kernels write into the owner's
+IPC-mapped buffers) and with point-to-point sends; the gathered outputs must
+equal the single-device run bit for bit (vectors, corrected frames, spatial
+and temporal summaries), with and without the A17 options, on two
+consecutive runs."""
 import os
 import socket
 
@@ -32,17 +34,21 @@ def _cfg(radius, L, m, win, shading):
                        shading_sigma=shading)
 
 
-def _worker(rank, world, port, raw, radius, L, m, win, shading, out_dir):
+def _worker(rank, world, port, raw, radius, L, m, win, shading, out_dir, exchange="peer"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         t, h, w = raw.shape
         s = distributed.balanced_plan(t, L, world, rank, win)
-        runner = distributed.BalancedShardedPreprocessor(h, w, _cfg(radius, L, m, win, shading))
+        runner = distributed.BalancedShardedPreprocessor(h, w, _cfg(radius, L, m, win, shading), exchange=exchange)
         local = D.as_device_frames(raw[s.local_lo:s.local_hi], torch.device("cuda", 0))
         corr = torch.empty((s.frames, h, w), dtype=torch.float32, device="cuda")
+        # two runs: the second reuses the exchange buffers (peer mode: ACK-ordered overwrite)
+        first = runner.run(local, s, m, corrected_out=corr)
+        first_tp = first.temporal.clone()
         res = runner.run(local, s, m, corrected_out=corr)
+        assert torch.equal(first_tp, res.temporal), "second run differs"
         vec = D.motion_to_numpy(res.vectors, res.n_frames)[s.frame_lo - s.local_lo:s.frame_hi - s.local_lo]
         np.savez(os.path.join(out_dir, f"r{rank}.npz"), vec=vec, sp=res.spatial.cpu().numpy(),
                  tp=res.temporal.cpu().numpy(), corr=corr.cpu().numpy(), lo=s.block_lo, hi=s.block_hi)
@@ -51,13 +57,16 @@ def _worker(rank, world, port, raw, radius, L, m, win, shading, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("T,L,W,m,win,shading", [
-    (600, 100, 4, 150, 0, 0.0),      # C2-like: 150-frame shards, blocks straddle every boundary
-    (300, 128, 5, 100, 0, 0.0),      # 60-frame shards: a block spans three ranks (middle role)
-    (500, 128, 3, 100, 33, 16.0),    # A17 high-pass halo + shading gain through the pieces
-    (122, 40, 2, 100, 0, 0.0),       # 2-frame final block
+@pytest.mark.parametrize("T,L,W,m,win,shading,exchange", [
+    (600, 100, 4, 150, 0, 0.0, "peer"),   # C2-like: 150-frame shards, blocks straddle every boundary
+    (600, 100, 4, 150, 0, 0.0, "p2p"),    # same, buffers sent point-to-point
+    (300, 128, 5, 100, 0, 0.0, "peer"),   # 60-frame shards: a block spans three ranks (middle relay)
+    (300, 128, 5, 100, 0, 0.0, "p2p"),
+    (500, 128, 3, 100, 33, 16.0, "peer"),  # A17 high-pass halo + shading gain through the pieces
+    (122, 40, 2, 100, 0, 0.0, "peer"),    # 2-frame final block
 ])
-def test_balanced_shards_equal_single_run(cuda, tmp_path, T, L, W, m, win, shading):
+@pytest.mark.timeout(300)
+def test_balanced_shards_equal_single_run(cuda, tmp_path, T, L, W, m, win, shading, exchange):
     cfg = synth.CONFIGS["c1"].with_frames(T)
     raw = synth.generate_numpy(cfg)
     pre = DevicePreprocessor(cfg.height, cfg.width, _cfg(cfg.radius, L, m, win, shading))
@@ -70,7 +79,7 @@ def test_balanced_shards_equal_single_run(cuda, tmp_path, T, L, W, m, win, shadi
     pre.close()
     del frames, corr_full
     torch.cuda.synchronize()
-    mp.start_processes(_worker, args=(W, _free_port(), raw, cfg.radius, L, m, win, shading, str(tmp_path)),
+    mp.start_processes(_worker, args=(W, _free_port(), raw, cfg.radius, L, m, win, shading, str(tmp_path), exchange),
                        nprocs=W, start_method="spawn")
     sp, tp, corr, vec = {}, {}, [], []
     for r in range(W):
