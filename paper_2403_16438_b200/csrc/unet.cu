@@ -268,7 +268,10 @@ int launch_conv(const ConvArgs& a, cudaStream_t s) {
 // 4w..4w+3) and fuses bias, ReLU, max-pool and the 1x1 + sigmoid.
 constexpr int kTcTH = 16, kTcTW = 16, kTcCB = kTcTW / 8;
 constexpr int kTcPH = kTcTH + 2, kTcPW = kTcTW + 2;
-constexpr int kTcPlane = kTcPH * kTcPW * 16;  // bytes of one 4-channel plane
+// bytes of one 4-channel plane, padded so the second channel-half plane starts
+// 28 banks further: the staging stores of 8 channels x 4 rows per warp then
+// hit 32 distinct banks
+constexpr int kTcPlane = kTcPH * kTcPW * 16 + 48;
 
 __device__ __forceinline__ uint64_t umma_sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
     return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
@@ -316,73 +319,86 @@ __global__ void __launch_bounds__(128) conv3x3_tc_kernel(ConvArgs a) {
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     const uint32_t tmem = tmem_base;
     const int nchunks = (a.cin + 7) / 8;
-    // stage chunk `ch`: weights by cp.async from their pre-split copy; the
-    // input tile row by row (a thread owns one (channel, padded row) pair at a
-    // time; the 16 interior samples of a row are 4 aligned float4 loads on the
-    // plain NCHW path), split hi / lo and stored K-major
-    auto stage = [&](int ch) {
-        unsigned char* sb = tc_smem;
-        const float* wsrc = a.wtc + (size_t)ch * (2 * kWBytes / 4);
-        for (int i = tid; i < 2 * kWBytes / 16; i += 128)
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(sb + 4 * kTcPlane + i * 16)),
-                         "l"(wsrc + i * 4)
-                         : "memory");
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    // Input chunks are software-pipelined through registers: the padded rows
+    // of chunk ch+1 are loaded (float4 interior, scalar halo) right after
+    // chunk ch's MMAs are issued, so their global latency hides behind the
+    // tensor cores; once those MMAs retire the rows are split hi / lo and
+    // stored K-major.  Weights cp.async from their pre-split copy.
+    constexpr int kRowsPerThread = (8 * kTcPH + 127) / 128;
+    float rows[kRowsPerThread][kTcPW];
+    auto load_rows = [&](int ch) {
         const int c0 = ch * 8;
-        for (int pr = tid; pr < 8 * kTcPH; pr += 128) {
-            const int ci = pr / kTcPH, yy = pr - ci * kTcPH;
+#pragma unroll
+        for (int k = 0; k < kRowsPerThread; ++k) {
+            const int pr = tid + 128 * k;
+#pragma unroll
+            for (int j = 0; j < kTcPW; ++j) rows[k][j] = 0.0f;
+            if (pr >= 8 * kTcPH) continue;
+            const int ci = pr & 7, yy = pr >> 3;  // lanes: 8 channels x 4 rows (conflict-free stores)
             const int y = oy0 + yy - 1, c = c0 + ci;
-            float row[kTcPW];
-#pragma unroll
-            for (int j = 0; j < kTcPW; ++j) row[j] = 0.0f;
-            if (c < a.cin && y >= 0 && y < a.h) {
-                const float* src = nullptr;
-                int step = 1;
-                if (c < a.c0) {
-                    if (a.mode == 0) {
-                        src = a.x0 + ((int64_t)n * a.c0 + c) * hw + (int64_t)y * a.w;
-                    } else if (a.mode == 1) {
-                        const int lw = a.w >> 1, lh = a.h >> 1;
-                        src = a.x0 + ((int64_t)n * a.c0 + c) * lh * lw + (int64_t)(y >> 1) * lw;
-                        step = 2;  // nearest upsample: column x reads x / 2
-                    } else {
-                        const int img = n / a.tiles_per_img;
-                        const int2 o = a.origins[n];
-                        src = a.x0 + (int64_t)img * a.img_stride + ((int64_t)c * a.ih + o.y + y) * a.iw + o.x;
-                    }
+            if (c >= a.cin || y < 0 || y >= a.h) continue;
+            const float* src = nullptr;
+            int step = 1;
+            if (c < a.c0) {
+                if (a.mode == 0) {
+                    src = a.x0 + ((int64_t)n * a.c0 + c) * hw + (int64_t)y * a.w;
+                } else if (a.mode == 1) {
+                    const int lw = a.w >> 1, lh = a.h >> 1;
+                    src = a.x0 + ((int64_t)n * a.c0 + c) * lh * lw + (int64_t)(y >> 1) * lw;
+                    step = 2;  // nearest upsample: column x reads x / 2
                 } else {
-                    src = a.x1 + ((int64_t)n * (a.cin - a.c0) + (c - a.c0)) * hw + (int64_t)y * a.w;
+                    const int img = n / a.tiles_per_img;
+                    const int2 o = a.origins[n];
+                    src = a.x0 + (int64_t)img * a.img_stride + ((int64_t)c * a.ih + o.y + y) * a.iw + o.x;
+                    step = 0;  // image tiles: arbitrary alignment
                 }
-                if (step == 1 && a.mode == 0 && c < a.c0 || (c >= a.c0)) {
-                    const float4* v4 = reinterpret_cast<const float4*>(src + ox0);  // ox0 % 16 == 0, w % 16 == 0
+            } else {
+                src = a.x1 + ((int64_t)n * (a.cin - a.c0) + (c - a.c0)) * hw + (int64_t)y * a.w;
+            }
+            if (step == 1) {  // NCHW rows: ox0 % 16 == 0 and w % 16 == 0 -> aligned float4
+                const float4* v4 = reinterpret_cast<const float4*>(src + ox0);
 #pragma unroll
-                    for (int q = 0; q < kTcTW / 4; ++q) {
-                        const float4 t = __ldg(v4 + q);
-                        row[1 + 4 * q] = t.x;
-                        row[2 + 4 * q] = t.y;
-                        row[3 + 4 * q] = t.z;
-                        row[4 + 4 * q] = t.w;
-                    }
-                    if (ox0 > 0) row[0] = __ldg(src + ox0 - 1);
-                    if (ox0 + kTcTW < a.w) row[kTcPW - 1] = __ldg(src + ox0 + kTcTW);
-                } else {
+                for (int q = 0; q < kTcTW / 4; ++q) {
+                    const float4 t = __ldg(v4 + q);
+                    rows[k][1 + 4 * q] = t.x;
+                    rows[k][2 + 4 * q] = t.y;
+                    rows[k][3 + 4 * q] = t.z;
+                    rows[k][4 + 4 * q] = t.w;
+                }
+                if (ox0 > 0) rows[k][0] = __ldg(src + ox0 - 1);
+                if (ox0 + kTcTW < a.w) rows[k][kTcPW - 1] = __ldg(src + ox0 + kTcTW);
+            } else {
 #pragma unroll
-                    for (int j = 0; j < kTcPW; ++j) {
-                        const int x = ox0 + j - 1;
-                        if (x >= 0 && x < a.w) row[j] = __ldg(src + (step == 2 ? (x >> 1) : x));
-                    }
+                for (int j = 0; j < kTcPW; ++j) {
+                    const int x = ox0 + j - 1;
+                    if (x >= 0 && x < a.w) rows[k][j] = __ldg(src + (step == 2 ? (x >> 1) : x));
                 }
             }
+        }
+    };
+    auto store_rows = [&]() {
+        unsigned char* sb = tc_smem;
+#pragma unroll
+        for (int k = 0; k < kRowsPerThread; ++k) {
+            const int pr = tid + 128 * k;
+            if (pr >= 8 * kTcPH) continue;
+            const int ci = pr & 7, yy = pr >> 3;
             unsigned char* dst = sb + (ci >> 2) * kTcPlane + yy * kTcPW * 16 + (ci & 3) * 4;
 #pragma unroll
             for (int j = 0; j < kTcPW; ++j) {
-                const float hi = tf32_hi(row[j]);
+                const float hi = tf32_hi(rows[k][j]);
                 *reinterpret_cast<float*>(dst + j * 16) = hi;
-                *reinterpret_cast<float*>(dst + 2 * kTcPlane + j * 16) = row[j] - hi;
+                *reinterpret_cast<float*>(dst + 2 * kTcPlane + j * 16) = rows[k][j] - hi;
             }
         }
-        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    };
+    auto fetch_w = [&](int ch) {
+        const float* wsrc = a.wtc + (size_t)ch * (2 * kWBytes / 4);
+        for (int i = tid; i < 2 * kWBytes / 16; i += 128)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(tc_smem + 4 * kTcPlane + i * 16)),
+                         "l"(wsrc + i * 4)
+                         : "memory");
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
     auto issue = [&](int ch) {
         const uint32_t sb = smem_u32(tc_smem);
@@ -408,19 +424,22 @@ __global__ void __launch_bounds__(128) conv3x3_tc_kernel(ConvArgs a) {
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
             smem_u32(&bar[0])));
     };
-    // one stage in shared memory (3 CTAs per SM overlap one another's staging
-    // and MMAs; a second stage per CTA was measured slower: 1-2 CTAs per SM)
     uint32_t ph = 0;
+    load_rows(0);
     for (int ch = 0; ch < nchunks; ++ch) {
-        if (ch > 0) {  // the previous chunk's MMAs have read the stage
+        if (ch > 0) {  // the previous chunk's MMAs have read the K-major planes and weights
             mbar_wait(&bar[0], ph);
             ph ^= 1u;
         }
-        stage(ch);
+        fetch_w(ch);
+        store_rows();
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;\n");
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         if (tid == 0) issue(ch);
+        if (ch + 1 < nchunks) load_rows(ch + 1);  // in flight during this chunk's MMAs
     }
     mbar_wait(&bar[0], ph);
     asm volatile("tcgen05.fence::after_thread_sync;\n");
