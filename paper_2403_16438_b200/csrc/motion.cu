@@ -115,7 +115,7 @@ struct ZnccArgs {
     int w;
     int P, R, S, tp;
     int nch;        // dx chunks per (patch, dy) item (1 on the fast path)
-    int rows;       // dy rows per patch in the item space (S; < S only in timing experiments)
+    int rows;       // lanes per patch in the item space: S, or 16 for the split S = 17 kernel
     int pitch_cap;  // f32 region pitch (odd, >= max wu)
     int bw, bh;     // raw box width / height in samples (bh = P + 2R)
     int bhc;        // TMA box height (the raw box is fetched as ceil(bh/bhc) row chunks)
@@ -855,8 +855,7 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     static const bool no_tma = getenv("VB_NO_TMA") != nullptr;  // debug toggle: plain-load staging
     a.use_tma = !no_tma && make_frames_tmap(&tmap, frames, dtype, n_frames, h, w, sp.bhc, sp.bw) ? 1 : 0;
 
-    static const char* hack_rows = getenv("VB_HACK_ROWS");  // timing experiment only: WRONG results
-    a.rows = split ? 16 : (hack_rows ? std::min(S, atoi(hack_rows)) : S);
+    a.rows = split ? 16 : S;
     const int items = fpi * t.max_g * a.rows * nch;
     // statistics kernel: one thread per union column (vertical chains), then
     // one per (patch, dy) row (horizontal chains)
