@@ -182,15 +182,20 @@ class DeviceUNet:
 
 
 _cache: dict[int, tuple[WeightBundle, DeviceUNet]] = {}
+_CACHE_MAX = 4  # device copies kept for the module-level functions (least recently used dropped)
 
 
 def _device_net(weights: WeightBundle) -> DeviceUNet:
-    hit = _cache.get(id(weights))
-    if hit is not None and hit[0] is weights:
-        return hit[1]
-    net = DeviceUNet(weights)
-    _cache[id(weights)] = (weights, net)
-    return net
+    """The uploaded copy of `weights` (keyed by identity: mutate a bundle's
+    tensors in place and the cached upload is stale -- build a DeviceUNet
+    explicitly for that)."""
+    hit = _cache.pop(id(weights), None)
+    if hit is None or hit[0] is not weights:
+        hit = (weights, DeviceUNet(weights))
+    _cache[id(weights)] = hit  # most recently used last
+    while len(_cache) > _CACHE_MAX:
+        _cache.pop(next(iter(_cache)))[1].close()
+    return hit[1]
 
 
 def _tile_count(height: int, width: int, stride: int = DEFAULT_STRIDE) -> int:
