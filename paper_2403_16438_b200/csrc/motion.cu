@@ -122,6 +122,9 @@ struct ZnccArgs {
     int use_tma;
     int tma_z0;     // tensor-map frame index of this launch's frame 0
     int off_reg, off_z, off_t;  // shared-memory carve-up (bytes); raw box at 0
+    int ss_pad;     // inv row stride per patch: S*S rounded to 4 floats (16-byte bulk copies)
+    int off_inv;    // search kernel: shared buffer receiving the group's inv rows (bulk copy), -1 = none
+    int conv_batch; // batched u16 -> f32 region conversion (all loads of a row first)
     int n_patches;
     const float* tmpl;
     const double* rvar;
@@ -284,7 +287,7 @@ __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __gri
                 h1 += r1[xx];
                 h2 += r2[xx];
             }
-            float* out = a.inv + ((size_t)t * a.n_patches + gp) * SS + (size_t)dy * S;
+            float* out = a.inv + ((size_t)t * a.n_patches + gp) * a.ss_pad + (size_t)dy * S;
 #pragma unroll
             for (int dx = 0; dx < (S_CT ? S_CT : 64); ++dx) {
                 if (!S_CT && dx >= S) break;
@@ -482,6 +485,8 @@ template <int P_CT, int S_CT, int FPI, bool SPLIT = false>
 __global__ void __launch_bounds__(SPLIT ? 128 : 288, SPLIT ? kSplitMinBlocks : 1) zncc_group_kernel(ZnccArgs a, const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar[FPI];
+    __shared__ __align__(8) uint64_t bar_inv;
+    uint32_t inv_phase = 0;
     const int P = P_CT ? P_CT : a.P;
     const int S = S_CT ? S_CT : a.S;
     const int R = (S - 1) / 2;
@@ -500,6 +505,7 @@ __global__ void __launch_bounds__(SPLIT ? 128 : 288, SPLIT ? kSplitMinBlocks : 1
     if (tid == 0 && a.use_tma) {
 #pragma unroll
         for (int f = 0; f < FPI; ++f) mbar_init(&bar[f], 1);
+        mbar_init(&bar_inv, 1);
         fence_mbar_init();
         tma_prefetch_desc(&tmap);
     }
@@ -528,7 +534,15 @@ __global__ void __launch_bounds__(SPLIT ? 128 : 288, SPLIT ? kSplitMinBlocks : 1
             for (int fr = tid >> 5; fr < nf * RH; fr += nw) {
                 const int f = fr / RH, r = fr - f * RH;
                 float* reg = reinterpret_cast<float*>(smem + a.off_reg + f * reg_slot) + r * pitch;
-                if (a.dtype == VB_U16) {
+                if (SPLIT && a.dtype == VB_U16 && wu <= 256 && a.conv_batch) {  // loads first, then converts (LDS latency overlapped)
+                    const uint16_t* raw = reinterpret_cast<const uint16_t*>(smem + f * raw_slot) + boff + r * a.bw;
+                    uint32_t v[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) v[k] = lane + 32 * k < wu ? raw[lane + 32 * k] : 0u;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        if (lane + 32 * k < wu) reg[lane + 32 * k] = u16_minus(v[k], magic);
+                } else if (a.dtype == VB_U16) {
                     const uint16_t* raw = reinterpret_cast<const uint16_t*>(smem + f * raw_slot) + boff + r * a.bw;
                     for (int c = lane; c < wu; c += 32) reg[c] = u16_minus(raw[c], magic);
                 } else {
@@ -539,6 +553,15 @@ __global__ void __launch_bounds__(SPLIT ? 128 : 288, SPLIT ? kSplitMinBlocks : 1
         }
         __syncthreads();
         if (t + FPI * gy < a.n_frames) fetch(t + FPI * gy);  // raw boxes are free
+        if (SPLIT && a.off_inv >= 0 && FPI == 1 && tid == 0) {  // this frame's inv rows land during the cross phase
+            const uint32_t bytes = (uint32_t)(G * a.ss_pad * 4);
+            mbar_expect_tx(&bar_inv, bytes);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                    smem_u32(smem + a.off_inv)),
+                "l"(a.inv + ((size_t)t * a.n_patches + grp.first) * a.ss_pad), "r"(bytes), "r"(smem_u32(&bar_inv))
+                : "memory");
+        }
         const int per_frame = G * a.rows * a.nch;
         const int nitems = nf * per_frame;
         // fast path: one item per thread, cov rows alias the dead regions;
@@ -623,14 +646,25 @@ __global__ void __launch_bounds__(SPLIT ? 128 : 288, SPLIT ? kSplitMinBlocks : 1
             }
         }
         __syncthreads();
+        const bool inv_smem = SPLIT && a.off_inv >= 0 && FPI == 1;
+        if (inv_smem) {  // the group's inv rows, bulk-copied during the cross phase
+            mbar_wait(&bar_inv, inv_phase);
+            inv_phase ^= 1u;
+        }
         for (int c2 = tid; c2 < nf * SS; c2 += nth) {
             const int ff = c2 / SS, c = c2 - ff * SS;
             const int64_t tf = t + ff * gy;
             const float* cov = cov_at(ff);
             double* part = a.partial + ((size_t)tf * a.n_groups + blockIdx.x) * SS;
-            const float* inv = a.inv + ((size_t)tf * a.n_patches + grp.first) * SS;
             double s = 0.0;
-            for (int q = 0; q < G; ++q) s += (double)cov[(size_t)q * SS + c] * (double)__ldg(inv + (size_t)q * SS + c);
+            if (inv_smem) {
+                const float* inv = reinterpret_cast<const float*>(smem + a.off_inv);
+                for (int q = 0; q < G; ++q) s += (double)cov[(size_t)q * SS + c] * (double)inv[(size_t)q * a.ss_pad + c];
+            } else {
+                const float* inv = a.inv + ((size_t)tf * a.n_patches + grp.first) * a.ss_pad;
+                for (int q = 0; q < G; ++q)
+                    s += (double)cov[(size_t)q * SS + c] * (double)__ldg(inv + (size_t)q * a.ss_pad + c);
+            }
             part[c] = s;
         }
     }
@@ -826,7 +860,16 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     SmemPlan sp = zncc_smem(patch, radius, t.max_g, t.max_wu, dtype, fpi, fast, t.pitch);
     if (std::max(sp.total, sp.stats_total) > 227 * 1024)
         return fail(VB_EINVAL, "patch group does not fit in shared memory");
-    VB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.total));
+    // the search kernel also receives the group's inv rows by bulk copy (fast path, one frame per iteration)
+    const int ss_pad_ = (S * S + 3) & ~3;
+    // measured on C2 (split kernel): 7.05 -> 6.78 ms with the conversion batching; kept to the
+    // split kernel -- the extra registers cost the generic S != 17 kernels a resident CTA
+    static const char* inv_mode = getenv("VB_INV_SMEM");  // experiment knob: 0 off
+    const bool want_inv = fast && fpi == 1 && patch == 21 && S == 17 && !(inv_mode && atoi(inv_mode) == 0);
+    const size_t inv_buf = want_inv ? (size_t)t.max_g * ss_pad_ * sizeof(float) : 0;
+    const size_t search_smem = ((sp.total + 15) & ~(size_t)15) + inv_buf;
+    if (search_smem > 227 * 1024) return fail(VB_EINVAL, "patch group does not fit in shared memory");
+    VB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)search_smem));
     VB_CUDA(cudaFuncSetAttribute(stats_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.stats_total));
 
     ZnccArgs a;
@@ -838,6 +881,10 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     a.S = S;
     a.tp = t.tp;
     a.nch = fast ? 1 : (S + kGenericDXB - 1) / kGenericDXB;
+    a.ss_pad = ss_pad_;
+    a.off_inv = -1;
+    static const char* cb = getenv("VB_CONV_BATCH");  // experiment knob
+    a.conv_batch = cb ? atoi(cb) : 1;
     a.pitch_cap = sp.pitch;
     a.bw = sp.bw;
     a.bh = sp.bh;
@@ -865,7 +912,7 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
 
     // frame batches bound the float64 partials + f32 inv buffers to ~1 GB
     const size_t per_frame_part = (size_t)t.n_groups * SS * sizeof(double);
-    const size_t per_frame_inv = (size_t)t.n * SS * sizeof(float);
+    const size_t per_frame_inv = (size_t)t.n * a.ss_pad * sizeof(float);
     int64_t batch = std::max<int64_t>(1, (int64_t)(((size_t)1 << 30) / (per_frame_part + per_frame_inv)));
     static const char* force_batch = getenv("VB_ZNCC_BATCH");  // experiment knob (frames per stats+search pair)
     if (force_batch && atoll(force_batch) > 0) batch = atoll(force_batch);
@@ -909,8 +956,9 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
             as.off_reg = (int)sp.off_reg;
             as.off_z = (int)sp.off_z;
             as.off_t = (int)sp.off_t;
+            as.off_inv = (inv_buf && a.use_tma) ? (int)((sp.total + 15) & ~(size_t)15) : -1;
             ProfScope ps(kProfZncc, s);
-            fn<<<grid, threads, sp.total, s>>>(as, tmap);
+            fn<<<grid, threads, search_smem, s>>>(as, tmap);
         }
         launches().fetch_add(1, std::memory_order_relaxed);
         e = cudaGetLastError();
