@@ -487,6 +487,9 @@ __global__ void __launch_bounds__(SPLIT ? 128 : 288, SPLIT ? kSplitMinBlocks : 1
     __shared__ __align__(8) uint64_t bar[FPI];
     __shared__ __align__(8) uint64_t bar_inv;
     uint32_t inv_phase = 0;
+    // inv bulk-copy path compiled for S = 17 (on) and S = 21 (off at run time: the variant with it
+    // compiled in measured faster on C5 either way); S = 25 keeps 96 registers without it
+    constexpr bool kInvPath = S_CT == 17 || S_CT == 21;
     const int P = P_CT ? P_CT : a.P;
     const int S = S_CT ? S_CT : a.S;
     const int R = (S - 1) / 2;
@@ -553,7 +556,7 @@ __global__ void __launch_bounds__(SPLIT ? 128 : 288, SPLIT ? kSplitMinBlocks : 1
         }
         __syncthreads();
         if (t + FPI * gy < a.n_frames) fetch(t + FPI * gy);  // raw boxes are free
-        if (SPLIT && a.off_inv >= 0 && FPI == 1 && tid == 0) {  // this frame's inv rows land during the cross phase
+        if (kInvPath && a.off_inv >= 0 && FPI == 1 && tid == 0) {  // this frame's inv rows land during the cross phase
             const uint32_t bytes = (uint32_t)(G * a.ss_pad * 4);
             mbar_expect_tx(&bar_inv, bytes);
             asm volatile(
@@ -646,7 +649,7 @@ __global__ void __launch_bounds__(SPLIT ? 128 : 288, SPLIT ? kSplitMinBlocks : 1
             }
         }
         __syncthreads();
-        const bool inv_smem = SPLIT && a.off_inv >= 0 && FPI == 1;
+        const bool inv_smem = kInvPath && a.off_inv >= 0 && FPI == 1;
         if (inv_smem) {  // the group's inv rows, bulk-copied during the cross phase
             mbar_wait(&bar_inv, inv_phase);
             inv_phase ^= 1u;
@@ -865,7 +868,8 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     // measured on C2 (split kernel): 7.05 -> 6.78 ms with the conversion batching; kept to the
     // split kernel -- the extra registers cost the generic S != 17 kernels a resident CTA
     static const char* inv_mode = getenv("VB_INV_SMEM");  // experiment knob: 0 off
-    const bool want_inv = fast && fpi == 1 && patch == 21 && S == 17 && !(inv_mode && atoi(inv_mode) == 0);
+    const bool want_inv = fast && fpi == 1 && !(inv_mode && atoi(inv_mode) == 0) &&
+                          (patch == 21 && S == 17 || (inv_mode && atoi(inv_mode) == 1));
     const size_t inv_buf = want_inv ? (size_t)t.max_g * ss_pad_ * sizeof(float) : 0;
     const size_t search_smem = ((sp.total + 15) & ~(size_t)15) + inv_buf;
     if (search_smem > 227 * 1024) return fail(VB_EINVAL, "patch group does not fit in shared memory");
