@@ -192,3 +192,20 @@ def test_c1_full_recording_vs_oracle(cuda, oracle_mod, monkeypatch):
     np.testing.assert_allclose(sub, ref["sub_conf"][:, :2], atol=1e-3, rtol=0)
     rel = np.abs(corrected.data - ref["corrected"]) / np.maximum(np.abs(ref["corrected"]), 1.0)
     assert rel.max() <= 1e-4
+
+
+@pytest.mark.parametrize("n_frames", [1, 2, 3, 5, 37])
+def test_c2_geometry_frame_counts_vs_oracle(cuda, oracle_mod, monkeypatch, n_frames):
+    """C2 geometry (256 x 512, r = 8: the split S = 17 search kernel, two frames
+    per CTA iteration) at frame counts that leave single-frame tails on some
+    CTAs: shifts, sub-pixel and corrected frames against the C oracle."""
+    cfg = synth.CONFIGS["c2"].with_frames(max(n_frames, 2))
+    raw = synth.generate_numpy(cfg)[:n_frames]
+    monkeypatch.setattr(motion, "REFERENCE_FRAMES", min(n_frames, 4))
+    corrected, vectors = correct_motion(Video(raw), MotionConfig(search_radius=cfg.radius))
+    ref = oracle_mod.preprocess(raw.astype(np.float32), 21, cfg.radius, True, min(n_frames, 4), 1000)
+    np.testing.assert_array_equal(np.array([[v.dx, v.dy] for v in vectors]), ref["dxdy"])
+    sub = np.array([[v.sub_dx, v.sub_dy] for v in vectors])
+    np.testing.assert_allclose(sub, ref["sub_conf"][:, :2], atol=1e-3, rtol=0)
+    rel = np.abs(corrected.data - ref["corrected"]) / np.maximum(np.abs(ref["corrected"]), 1.0)
+    assert rel.max() <= 1e-4
