@@ -741,6 +741,272 @@ static int launch_k3_tma(const CUtensorMap& tmap, K3Args a, int64_t n, int h, in
     return VB_OK;
 }
 
+// ---------------------------------------------------------- K3, split form
+// The fused kernel above interpolates the corrected tile + halo (2x the
+// tile's pixels) in every CTA, and those f32 phases cost as many issue slots
+// as the float64 passes.  The split form writes the corrected frames once
+// (K3a: a streaming kernel, every pixel interpolated once, in numpy's order)
+// and the smoothing kernel (K3b) stages each corrected tile + halo with one
+// TMA box into shared memory -- double-buffered, the next frame's box lands
+// while this frame's passes run -- mirrors the reflected halo inside the box
+// at the frame edges, and runs the same two float64 passes.  Same arithmetic,
+// so the results are bit-identical to the fused kernel.
+constexpr int kCW = 8;  // K3a: corrected outputs per thread (one row segment)
+constexpr int kK3NotHandled = -100;  // launch_k3_split: use the fused kernel instead
+
+// One thread: a strip of kCW columns x kCR rows.  translate's top row of
+// output y is the bottom row of output y + 1 (both clamp(y - iy)), so each
+// horizontal interpolation serves two outputs: kCR + 1 per strip.
+constexpr int kCR = 8;
+
+template <bool U16>
+__global__ void __launch_bounds__(256) correct_rows_kernel(const void* __restrict__ frames, int64_t n, int h, int w,
+                                                           const vb_motion* __restrict__ vec,
+                                                           const float* __restrict__ gain, float* __restrict__ out) {
+    using S_T = typename std::conditional<U16, uint16_t, float>::type;
+    const int64_t hw = (int64_t)h * w;
+    const int wq = (w + kCW - 1) / kCW, hq = (h + kCR - 1) / kCR;
+    const int per_frame = hq * wq;
+    for (int64_t t = blockIdx.y; t < n; t += gridDim.y) {
+        const WarpOp op = make_warp(vec, t);
+        const S_T* f = reinterpret_cast<const S_T*>(frames) + t * hw;
+        float* o = out + t * hw;
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < per_frame; i += gridDim.x * blockDim.x) {
+            const int yb = (i / wq) * kCR, x0 = (i - (i / wq) * wq) * kCW;
+            // source columns x - ix - 1 + j, j = 0..kCW (b taps at j, a taps at j + 1)
+            const int c0 = x0 - op.ix - 1;
+            const bool inner = c0 >= 0 && c0 + kCW < w;
+            // raw samples of a source row; the next row's loads are issued before
+            // this row's arithmetic (one row of look-ahead)
+            auto load_row = [&](int r, S_T (&raw)[kCW + 1]) {
+                const S_T* row = f + (int64_t)r * w;
+#pragma unroll
+                for (int j = 0; j <= kCW; ++j) raw[j] = __ldg(row + (inner ? c0 + j : clampi(c0 + j, 0, w - 1)));
+            };
+            auto hrow = [&](const S_T (&raw)[kCW + 1], float (&hv)[kCW]) {  // horizontal interpolation
+                float v[kCW + 1];
+#pragma unroll
+                for (int j = 0; j <= kCW; ++j) {
+                    if constexpr (U16)
+                        v[j] = u16_minus(raw[j], 8388608.0f);  // exact widening on the FMA pipe
+                    else
+                        v[j] = raw[j];
+                }
+#pragma unroll
+                for (int k = 0; k < kCW; ++k) hv[k] = __fadd_rn(__fmul_rn(op.omx, v[k + 1]), __fmul_rn(op.fx, v[k]));
+            };
+            S_T rc_raw[kCW + 1], ra_raw[kCW + 1];
+            load_row(clampi(yb - op.iy - 1, 0, h - 1), rc_raw);
+            load_row(clampi(yb - op.iy, 0, h - 1), ra_raw);
+            float hc[kCW], ha[kCW];
+            hrow(rc_raw, hc);
+#pragma unroll 1
+            for (int y = yb; y < yb + kCR && y < h; ++y) {
+                S_T cur[kCW + 1];
+#pragma unroll
+                for (int j = 0; j <= kCW; ++j) cur[j] = ra_raw[j];
+                if (y + 1 < yb + kCR && y + 1 < h) load_row(clampi(y + 1 - op.iy, 0, h - 1), ra_raw);
+                hrow(cur, ha);
+                float v[kCW];
+#pragma unroll
+                for (int k = 0; k < kCW; ++k) {
+                    v[k] = __fadd_rn(__fmul_rn(op.omy, ha[k]), __fmul_rn(op.fy, hc[k]));
+                    if (gain && x0 + k < w) v[k] = __fdiv_rn(v[k], __ldg(gain + (int64_t)y * w + x0 + k));
+                    hc[k] = ha[k];
+                }
+                float* dst = o + (int64_t)y * w + x0;
+                if ((w & 3) == 0 && x0 + kCW <= w) {
+#pragma unroll
+                    for (int k = 0; k < kCW; k += 4)
+                        *reinterpret_cast<float4*>(dst + k) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < kCW; ++k)
+                        if (x0 + k < w) dst[k] = v[k];
+                }
+            }
+        }
+    }
+}
+
+template <int WR>
+struct K3bGeom {
+    static constexpr int EH = kTY + 2 * WR, EW = kTX + 2 * WR, EWP = EW | 1;
+    static constexpr int XO = (4 - WR % 4) % 4;      // box starts at the 16-byte aligned column tx0 - WR - XO
+    static constexpr int BW = (EW + XO + 3) / 4 * 4;  // box width (f32), a 16-byte multiple
+    static constexpr int BH = EH + 1;  // one spare row: the last vertical segment loads rows up to EH unguarded
+    static constexpr size_t box_bytes = ((size_t)BH * BW * sizeof(float) + 127) & ~(size_t)127;  // TMA dst: 128-B aligned
+    static constexpr size_t smem = 2 * box_bytes + (size_t)(kTY + 1) * EWP * sizeof(float);
+};
+
+template <int WR>
+__global__ void __launch_bounds__(kK3Threads, kK3V2MinBlocks) smooth_tma_kernel(K3Args a, const __grid_constant__ CUtensorMap tmap) {
+    using G = K3bGeom<WR>;
+    constexpr int EH = G::EH, EW = G::EW, EWP = G::EWP, XO = G::XO, BW = G::BW;
+    extern __shared__ __align__(128) unsigned char smem[];
+    float* sBox = reinterpret_cast<float*>(smem);                  // 2 x [EH][BW] corrected tile + halo
+    float* sV = reinterpret_cast<float*>(smem + 2 * G::box_bytes);  // [kTY][EWP] vertical pass
+    __shared__ __align__(8) uint64_t bar[2];
+    const int tid = threadIdx.x;
+    const int ty0 = blockIdx.y * kTY, tx0 = blockIdx.x * kTX;
+    const int64_t hw = (int64_t)a.h * a.w;
+    const int y_lo = ty0 - WR, x_lo = tx0 - WR;
+    // tiles whose halo leaves the frame mirror it inside the box (scipy "reflect")
+    const bool edge = y_lo < 0 || x_lo < 0 || ty0 + kTY + WR > a.h || tx0 + kTX + WR > a.w;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+        tma_prefetch_desc(&tmap);
+    }
+    __syncthreads();
+    auto issue = [&](int64_t t, int b) {
+        mbar_expect_tx(&bar[b], (uint32_t)(G::BH * BW * sizeof(float)));
+        tma_load_3d(sBox + b * (G::box_bytes / sizeof(float)), &tmap, x_lo - XO, y_lo, (int)t, &bar[b]);
+    };
+    int64_t t = blockIdx.z;
+    if (tid == 0) {
+        if (t < a.n) issue(t, 0);
+        if (t + gridDim.z < a.n) issue(t + gridDim.z, 1);
+    }
+    uint32_t phase[2] = {0u, 0u};
+    for (int i = 0; t < a.n; t += gridDim.z, ++i) {
+        const int b = i & 1;
+        float* sC = sBox + b * (G::box_bytes / sizeof(float));
+        mbar_wait(&bar[b], phase[b]);
+        phase[b] ^= 1u;
+        if (edge) {
+            // halo columns outside the frame first (every row), then halo rows
+            // (whole rows), so corners mirror twice
+            const int nl = max(0, -x_lo), nr = max(0, x_lo + EW - a.w), nc = nl + nr;
+            for (int k = tid; k < EH * nc; k += kK3Threads) {
+                const int ey = k / nc, j = k - ey * nc;
+                const int ex = j < nl ? j : EW - nr + (j - nl);
+                const int sx = clampi(reflect_index(x_lo + ex, a.w) - x_lo, 0, EW - 1);
+                sC[ey * BW + XO + ex] = sC[ey * BW + XO + sx];
+            }
+            __syncthreads();
+            const int nt = max(0, -y_lo), nb = max(0, y_lo + EH - a.h), nrw = nt + nb;
+            for (int k = tid; k < nrw * EW; k += kK3Threads) {
+                const int j = k / EW, ex = k - j * EW;
+                const int ey = j < nt ? j : EH - nb + (j - nt);
+                const int sy = clampi(reflect_index(y_lo + ey, a.h) - y_lo, 0, EH - 1);
+                sC[ey * BW + XO + ex] = sC[sy * BW + XO + ex];
+            }
+        }
+        __syncthreads();  // box (mirrored) complete; the previous frame's horizontal pass is done with sV
+        // B: vertical 19-tap pass, (column, third of the rows) per thread
+        if (tid < 3 * EW) {
+            const int c = tid % EW, seg = tid / EW;
+            const int r0 = seg * kVR2;
+            const int nout = seg < 2 ? kVR2 : kTY - 2 * kVR2;
+            double x[kVR2 + 2 * WR];
+            static_assert(2 * kVR2 + kVR2 + 2 * WR <= EH + 1, "box rows cover every segment's loads");
+#pragma unroll
+            for (int q = 0; q < kVR2 + 2 * WR; ++q) x[q] = (double)sC[(r0 + q) * BW + XO + c];
+            double acc[kVR2];
+#pragma unroll
+            for (int j = 0; j < kVR2; ++j) acc[j] = __dmul_rn(x[j + WR], a.wt.w[WR]);
+#pragma unroll
+            for (int k = WR; k >= 1; --k) {
+#pragma unroll
+                for (int j = 0; j < kVR2; ++j)
+                    acc[j] = __dadd_rn(acc[j], __dmul_rn(__dadd_rn(x[j + WR - k], x[j + WR + k]), a.wt.w[WR - k]));
+            }
+            (void)nout;  // the last segment's 11th row lands in sV's spare row
+#pragma unroll
+            for (int j = 0; j < kVR2; ++j) sV[(r0 + j) * EWP + c] = (float)acc[j];
+        }
+        __syncthreads();  // sV complete; this box is free
+        if (tid == 0 && t + 2 * (int64_t)gridDim.z < a.n) issue(t + 2 * (int64_t)gridDim.z, b);
+        // C: horizontal pass -> smoothed frame.  Lanes take consecutive rows.
+        {
+            constexpr int HR = 8;
+            const int ly = tid % kTY, lx0 = (tid / kTY) * HR;
+            double x[HR + 2 * WR];
+#pragma unroll
+            for (int q = 0; q < HR + 2 * WR; ++q) x[q] = (double)sV[ly * EWP + lx0 + q];
+            double acc[HR];
+#pragma unroll
+            for (int j = 0; j < HR; ++j) acc[j] = __dmul_rn(x[j + WR], a.wt.w[WR]);
+#pragma unroll
+            for (int k = WR; k >= 1; --k) {
+#pragma unroll
+                for (int j = 0; j < HR; ++j)
+                    acc[j] = __dadd_rn(acc[j], __dmul_rn(__dadd_rn(x[j + WR - k], x[j + WR + k]), a.wt.w[WR - k]));
+            }
+            float o[HR];
+#pragma unroll
+            for (int j = 0; j < HR; ++j) o[j] = (float)acc[j];
+            const int gy = ty0 + ly, gx0 = tx0 + lx0;
+            float* dst = a.smoothed + t * hw + (int64_t)gy * a.w + gx0;
+            if (gy < a.h) {
+                if ((a.w & 3) == 0 && gx0 + HR <= a.w) {
+#pragma unroll
+                    for (int j = 0; j < HR; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < HR; ++j)
+                        if (gx0 + j < a.w) dst[j] = o[j];
+                }
+            }
+        }
+    }
+}
+
+// Split K3 for radius 9: K3a into `corrected` (or a scratch buffer), then K3b.
+// Returns kK3NotHandled (the caller falls back to the fused kernel) when the tensor
+// map cannot describe the corrected frames.
+static int launch_k3_split(const void* frames, int dtype, const vb_motion* vec, int64_t n, int h, int w,
+                           const K3Args& base, float* corrected, float* smoothed, cudaStream_t s) {
+    using G = K3bGeom<9>;
+    if ((w & 3) || n > 0x7fffffff || h < 10 || w < 10) return kK3NotHandled;
+    float* corr = corrected;
+    float* tmp = nullptr;
+    const int64_t hw = (int64_t)h * w;
+    if (!corr) {
+        keep_pool();
+        VB_CUDA(cudaMallocAsync(&tmp, (size_t)n * hw * sizeof(float), s));
+        corr = tmp;
+    }
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof(tmap));
+    if (!make_frames_tmap(&tmap, corr, VB_F32, n, h, w, G::BH, G::BW)) {
+        if (tmp) cudaFreeAsync(tmp, s);
+        return kK3NotHandled;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    {
+        const int wq = (w + kCW - 1) / kCW;
+        const int per_frame = ((h + kCR - 1) / kCR) * wq;
+        const int bx = std::max(1, std::min((per_frame + 255) / 256, 64));
+        const int64_t gy = std::min<int64_t>(65535, std::min<int64_t>(n, std::max<int64_t>(1, (int64_t)sms * 8 / bx)));
+        dim3 grid((unsigned)bx, (unsigned)gy);
+        ProfScope ps(kProfWarpSmooth, s);
+        if (dtype == VB_U16)
+            correct_rows_kernel<true><<<grid, 256, 0, s>>>(frames, n, h, w, vec, base.gain, corr);
+        else
+            correct_rows_kernel<false><<<grid, 256, 0, s>>>(frames, n, h, w, vec, base.gain, corr);
+    }
+    VB_LAUNCHED();
+    K3Args a = base;
+    a.n = n;
+    a.smoothed = smoothed;
+    VB_CUDA(cudaFuncSetAttribute(smooth_tma_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::smem));
+    const int tiles = ((w + kTX - 1) / kTX) * ((h + kTY - 1) / kTY);
+    const int64_t gz = std::min<int64_t>(65535, std::max<int64_t>((n + 3) / 4, ((int64_t)sms * 24 + tiles - 1) / tiles));
+    dim3 grid((unsigned)((w + kTX - 1) / kTX), (unsigned)((h + kTY - 1) / kTY), (unsigned)std::min<int64_t>(gz, n));
+    {
+        ProfScope ps(kProfWarpSmooth, s);
+        smooth_tma_kernel<9><<<grid, kK3Threads, G::smem, s>>>(a, tmap);
+    }
+    VB_LAUNCHED();
+    if (tmp) cudaFreeAsync(tmp, s);
+    return VB_OK;
+}
+
 // Spatial summary (summarize.py:55-57): per-pixel float64 mean over the
 // block's corrected frames, accumulated sequentially in frame order like
 // numpy's axis-0 reduction -> bit-identical.
@@ -1135,6 +1401,11 @@ static int launch_k3(const void* frames, int dtype, const vb_motion* vec, int64_
     a.gain = gain;
     for (int i = 0; i < 2 * wradius + 1; ++i) a.wt.w[i] = weights[i];
     static const bool no_tma = getenv("VB_NO_TMA") != nullptr;
+    static const char* k3_mode = getenv("VB_K3_SPLIT");  // experiment knob: 0 = fused kernel
+    if (wradius == 9 && !no_tma && !(k3_mode && atoi(k3_mode) == 0)) {
+        const int rc = launch_k3_split(frames, dtype, vec, n, h, w, a, corrected, smoothed, s);
+        if (rc != kK3NotHandled) return rc;
+    }
     if (wradius == 9 && !no_tma && n <= 0x7fffffff) {
         constexpr int EH = kTY + 18, EW = kTX + 18;
         CUtensorMap tmap;

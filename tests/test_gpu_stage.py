@@ -261,3 +261,24 @@ def test_preprocess_file_streams_from_disk(cuda, tmp_path, c1_small, sample):
     np.testing.assert_array_equal(vec["sub_dy"], [v.sub_dy for v in vectors])
     np.testing.assert_array_equal(sp, np.stack([p.spatial for p in pairs]))
     np.testing.assert_array_equal(tp, np.stack([p.temporal for p in pairs]))
+
+
+@pytest.mark.parametrize("shape", [(100, 124), (70, 68), (37, 44)])
+def test_partial_tiles_warp_and_smooth_vs_oracle(cuda, oracle_mod, c1_small, shape):
+    """Frame sizes that leave partial 32 x 64 tiles and mirrored halos on every
+    side (the split warp -> TMA-staged smoothing path): corrected frames
+    bit-exact against the oracle's translate with this run's vectors, and the
+    summaries bit-exact against the oracle's on those corrected frames."""
+    cfg, raw = c1_small
+    h, w = shape
+    v = np.ascontiguousarray(raw[:120, 3:3 + h, 5:5 + w])
+    r = 3 if min(h, w) < 60 else cfg.radius
+    corrected, vectors, pairs = preprocess(Video(v), StageConfig(search_radius=r, segment_length=40, ref_frames=20))
+    f = v.astype(np.float32)
+    for t in range(0, len(vectors), 7):
+        vec = vectors[t]
+        np.testing.assert_array_equal(corrected.data[t], oracle_mod.correct_frame(f[t], vec.dx + vec.sub_dx, vec.dy + vec.sub_dy))
+    for i, p in enumerate(pairs):
+        blk = corrected.data[40 * i:40 * (i + 1)]
+        np.testing.assert_array_equal(p.spatial, oracle_mod.spatial_summary(blk))
+        np.testing.assert_array_equal(p.temporal, oracle_mod.temporal_summary(blk))

@@ -57,7 +57,8 @@ class TestGaussian:  # test_summarize.py:75-95
         with pytest.raises(ValueError):
             gaussian_smooth(np.zeros((4, 4)), 0.0)
 
-    @pytest.mark.parametrize("shape", [(31, 29), (8, 8), (4, 4), (1, 5), (256, 512), (70, 130)])
+    @pytest.mark.parametrize("shape", [(31, 29), (8, 8), (4, 4), (1, 5), (256, 512), (70, 130),
+                                       (70, 132), (100, 68), (36, 12), (10, 12), (9, 16), (33, 100)])
     def test_bit_exact_vs_scipy(self, cuda, rng, shape):
         x = (rng.random(shape, dtype=np.float32) * 1000).astype(np.float32)
         want = ndimage.gaussian_filter1d(ndimage.gaussian_filter1d(x, 3.0, axis=0, mode="reflect", radius=9),
@@ -155,9 +156,11 @@ class TestSummarize:  # test_summarize.py:150-187
             np.testing.assert_array_equal(p.spatial, q.spatial)
             np.testing.assert_array_equal(p.temporal, q.temporal)
 
-    def test_large_frame_tiles_vs_oracle(self, cuda, oracle_mod, rng):
-        """Frame sizes that are not multiples of the 32x64 tile."""
-        v = (rng.random((40, 70, 131), dtype=np.float32) * 1000).astype(np.float32)
+    @pytest.mark.parametrize("shape", [(70, 131), (70, 132), (100, 68)])
+    def test_large_frame_tiles_vs_oracle(self, cuda, oracle_mod, rng, shape):
+        """Frame sizes that are not multiples of the 32x64 tile (w % 4 == 0:
+        the split warp -> TMA smoothing path; otherwise the fused kernel)."""
+        v = (rng.random((40, *shape), dtype=np.float32) * 1000).astype(np.float32)
         pairs = summarize(Video(v), 20)
         for i, p in enumerate(pairs):
             np.testing.assert_array_equal(p.spatial, oracle_mod.spatial_summary(v[20 * i:20 * (i + 1)]))
