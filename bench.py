@@ -363,8 +363,8 @@ def run_ours(args):
     hbm_stage = bytes_frame * total_frames / world / (step_ms / 1e3) / 1e9
     roofline = {
         "bound": "fp32",
-        "kernel": ("zncc_group_kernel<21,17,1,split>: half-warp per patch, shared middle row" if cfg.radius == 8
-                   else f"zncc_group_kernel<21,{2 * cfg.radius + 1},1>"),
+        "kernel": ("zncc_group_kernel<21,17,2,split>: half-warp per patch, shared middle row, two frames per "
+                   "thread through FFMA2" if cfg.radius == 8 else f"zncc_group_kernel<21,{2 * cfg.radius + 1},1>"),
         "plan": pre.plan.info(),
         "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
         "traffic": traffic,

@@ -9,6 +9,6 @@ $CMD > $OUT/prof_plain_$TAG.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv $CMD > $OUT/ncu_launch_$TAG.log 2>&1
 echo "launch list rc=$?"
 $CMD > $OUT/prof_plain2_$TAG.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"zncc|warp_smooth|median|block_mean" -s 5 -c 5 \
+ncu --set full --clock-control none --import-source on -k regex:"zncc|smooth|correct_rows|median|block_mean" -s 6 -c 6 \
     -o $OUT/prof_$TAG -f $CMD > $OUT/ncu_full_$TAG.log 2>&1
 echo "full rc=$?"

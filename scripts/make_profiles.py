@@ -60,7 +60,7 @@ def main(tag: str, frames_per_launch: int = 2000):
     with redirect_stdout(buf):
         print(f"ncu --set full --clock-control none of `{CMD}` (one launch per kernel, {frames_per_launch} frames)")
         ncu_summary.main(rep)
-        for k in ("zncc_group", "zncc_stats", "warp_smooth", "median"):
+        for k in ("zncc_group", "zncc_stats", "smooth_tma", "correct_rows", "median"):
             print(f"\n-- warp-stall samples, {k}")
             try:
                 ncu_stalls.main(rep, k, 12)
