@@ -548,10 +548,10 @@ __global__ void __launch_bounds__(SPLIT ? 128 : 288, SPLIT ? (FPI == 2 ? 2 : kSp
             phase ^= 1u;
         }
         // raw boxes -> centred f32 regions: warps over rows, lanes over columns
-        // (split kernels: threads over (frame, column) units walking all rows,
-        // eight loads in flight, no per-row index arithmetic)
-        if (SPLIT && a.dtype == VB_U16 && a.conv_batch == 2) {
-            constexpr int RHC = SPLIT ? P_CT + S_CT - 1 : 1;
+        // (compile-time-S kernels: threads over (frame, column) units walking
+        // all rows, eight loads in flight, no per-row index arithmetic)
+        if (S_CT != 0 && a.dtype == VB_U16 && a.conv_batch >= 2) {
+            constexpr int RHC = S_CT != 0 ? P_CT + S_CT - 1 : 1;
             for (int u = tid; u < nf * wu; u += nth) {
                 const int f = u >= wu ? 1 : 0, c = u - f * wu;
                 const uint16_t* raw = reinterpret_cast<const uint16_t*>(smem + f * raw_slot) + boff + c;
@@ -977,7 +977,8 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     a.ss_pad = ss_pad_;
     a.off_inv = -1;
     static const char* cb = getenv("VB_CONV_BATCH");  // experiment knob
-    // 2: split kernels convert column-major (measured 6.90 -> 6.62 ms per 4000 C2 frames)
+    // 2: compile-time-S kernels convert column-major (measured per search: C2 6.90 -> 6.62 ms per
+    // 4000 frames, C3 14.74 -> 13.55 ms per 2000, C5 20.91 -> 19.81 ms per 1000)
     a.conv_batch = cb ? atoi(cb) : 2;
     a.pitch_cap = sp.pitch;
     a.bw = sp.bw;
