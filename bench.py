@@ -363,6 +363,9 @@ def run_ours(args):
     hbm_stage = bytes_frame * total_frames / world / (step_ms / 1e3) / 1e9
     roofline = {
         "bound": "fp32",
+        "bound_note": ("neither 'hbm' nor 'tensor': the dominant kernel is bound by the FP32 FMA pipe (ZNCC cross "
+                       "sums, SURVEY 8(d)); the whole stage moves a few % of HBM bandwidth (roofline.hbm); a "
+                       "per-patch template is an N = 1 product, so tensor cores do not apply"),
         "kernel": ("zncc_group_kernel<21,17,2,split>: half-warp per patch, shared middle row, two frames per "
                    "thread through FFMA2" if cfg.radius == 8 else f"zncc_group_kernel<21,{2 * cfg.radius + 1},1>"),
         "plan": pre.plan.info(),
