@@ -215,6 +215,24 @@ __device__ __forceinline__ double rsqrt_pos(double x) {
     return y * fma(-0.5 * x * y, y, 1.5);
 }
 
+// One inv row of S values whose first element sits K floats past a 16-byte
+// boundary (inv rows are dense, S floats apart; per-patch blocks start
+// 16-byte aligned): (4 - K) & 3 scalar stores, float4 stores, scalar tail --
+// 6 stores instead of 17 for S = 17 (measured: the scalar stores, each warp
+// store touching 32 sectors, were 18 % of the statistics kernel).
+template <int S, int K>
+__device__ __forceinline__ void store_row(float* out, const float (&v)[S]) {
+    constexpr int head = (4 - K) & 3, nv = (S - head) / 4;
+#pragma unroll
+    for (int i = 0; i < head && i < S; ++i) out[i] = v[i];
+#pragma unroll
+    for (int q = 0; q < nv; ++q)
+        reinterpret_cast<float4*>(out + head)[q] =
+            make_float4(v[head + 4 * q], v[head + 4 * q + 1], v[head + 4 * q + 2], v[head + 4 * q + 3]);
+#pragma unroll
+    for (int i = head + 4 * nv; i < S; ++i) out[i] = v[i];
+}
+
 template <bool INT, int P_CT, int S_CT = 0>
 __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __grid_constant__ CUtensorMap tmap) {
     using T1 = typename std::conditional<INT, int, double>::type;        // sample / sum of f
@@ -273,7 +291,26 @@ __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __gri
         __syncthreads();
         if (t + gridDim.y < a.n_frames) fetch_box(a, &tmap, grp, t + gridDim.y, smem, &bar);  // raw box is free
         for (int it = threadIdx.x; it < G * S; it += blockDim.x) {
-            const int p = it / S, dy = it - p * S;
+            int p, dy;
+            if constexpr (S_CT != 0) {
+                // items ordered by the 16-byte phase k = (dy * S) & 3 of their inv row, so a
+                // warp's rows share the phase and store as (head, float4s, tail) together
+                // (class k holds dy = d0, d0 + 4, ... with d0 = (k*S) & 3: S odd, S*S = 1 mod 4)
+                int k = 0, idx = it;
+#pragma unroll
+                for (int kk = 0; kk < 3; ++kk) {
+                    const int nk = (S_CT - ((kk * S_CT) & 3) + 3) / 4;
+                    if (idx < G * nk) break;
+                    idx -= G * nk;
+                    k = kk + 1;
+                }
+                const int d0 = (k * S_CT) & 3, nk = (S_CT - d0 + 3) / 4;
+                p = idx / nk;
+                dy = d0 + 4 * (idx - p * nk);
+            } else {
+                p = it / S;
+                dy = it - p * S;
+            }
             const int gp = grp.first + p;
             const int col = a.patch_col[gp];
             const double rv = a.rvar[gp];
@@ -288,6 +325,7 @@ __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __gri
                 h2 += r2[xx];
             }
             float* out = a.inv + ((size_t)t * a.n_patches + gp) * a.ss_pad + (size_t)dy * S;
+            float ivs[S_CT ? S_CT : 1];
 #pragma unroll
             for (int dx = 0; dx < (S_CT ? S_CT : 64); ++dx) {
                 if (!S_CT && dx >= S) break;
@@ -304,10 +342,21 @@ __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __gri
                     const double fvar = h2 - h1 * h1 / nn;  // kernels.py:67
                     if (rv > 0.0 && fvar > 0.0) iv = (float)rsqrt(fvar * rv);
                 }
-                out[dx] = iv;
+                if constexpr (S_CT != 0)
+                    ivs[dx] = iv;
+                else
+                    out[dx] = iv;
                 if (dx + 1 < S) {
                     h1 += r1[dx + P] - r1[dx];
                     h2 += r2[dx + P] - r2[dx];
+                }
+            }
+            if constexpr (S_CT != 0) {
+                switch ((dy * S_CT) & 3) {  // warp-uniform except where two phases meet
+                    case 0: store_row<S_CT, 0>(out, ivs); break;
+                    case 1: store_row<S_CT, 1>(out, ivs); break;
+                    case 2: store_row<S_CT, 2>(out, ivs); break;
+                    default: store_row<S_CT, 3>(out, ivs); break;
                 }
             }
         }
