@@ -366,12 +366,16 @@ __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __gri
 // Cross sums for one (patch, dy) row of S candidates, compile-time P and S.
 // Template taps come from the prepared patch in global memory (L1-resident,
 // warp-broadcast): every lane of a patch reads the same float4.
+#ifndef VB_GEN_UNROLL
+#define VB_GEN_UNROLL 1  // measured: 2 -> C3 search 13.54 -> 16.75 ms (115 registers)
+#endif
+constexpr int kGenUnroll = VB_GEN_UNROLL;
 template <int P, int S>
 __device__ __forceinline__ void cross_row(const float* __restrict__ reg, int pitch, const float* __restrict__ trow0,
                                           int tp, float (&acc)[S]) {
 #pragma unroll
     for (int d = 0; d < S; ++d) acc[d] = 0.0f;
-#pragma unroll 1
+#pragma unroll kGenUnroll
     for (int yy = 0; yy < P; ++yy) {
         const float* fr = reg + yy * pitch;
         float win[S + P - 1];
@@ -410,9 +414,13 @@ __device__ __forceinline__ void cross_row(const float* __restrict__ reg, int pit
 // loaded for the lane's own row serves the shared row too.  The half-warp
 // then sums the shared row's partials in a fixed shuffle tree.
 #ifndef VB_SPLIT_UNROLL
-#define VB_SPLIT_UNROLL 1  // measured: 3 -> 7.41 ms, 7 -> 9.16 ms (instruction cache) vs 7.12 ms
+#define VB_SPLIT_UNROLL 1  // one frame per thread, measured: 3 -> 7.41 ms, 7 -> 9.16 ms (instruction cache) vs 7.12 ms
+#endif
+#ifndef VB_SPLIT_UNROLL_PAIR
+#define VB_SPLIT_UNROLL_PAIR 2  // two frames per thread (half the FMA instructions), measured: 6.28 -> 5.89 ms (2, 3 or 7 alike)
 #endif
 constexpr int kSplitUnroll = VB_SPLIT_UNROLL;
+constexpr int kSplitUnrollPair = VB_SPLIT_UNROLL_PAIR;
 #ifndef VB_SPLIT_PREFETCH
 #define VB_SPLIT_PREFETCH 4  // measured: 7.57 -> 7.29 ms per 4000 C2 frames (4 or 8 samples alike)
 #endif
@@ -463,7 +471,8 @@ __device__ __forceinline__ void cross_row_split17(const float* __restrict__ reg,
 #pragma unroll
     for (int i = 0; i < PF; ++i) lane_load(w_next[i], reg + i, fstride);
 #endif
-#pragma unroll kSplitUnroll
+    constexpr int kUnroll = std::is_same<V, float2>::value ? kSplitUnrollPair : kSplitUnroll;
+#pragma unroll kUnroll
     for (int yy = 0; yy < P; ++yy) {
         const float* fr = reg + yy * pitch;
         V win[S + P - 1];
