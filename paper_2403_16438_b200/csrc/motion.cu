@@ -421,6 +421,9 @@ __device__ __forceinline__ void cross_row(const float* __restrict__ reg, int pit
 #endif
 constexpr int kSplitUnroll = VB_SPLIT_UNROLL;
 constexpr int kSplitUnrollPair = VB_SPLIT_UNROLL_PAIR;
+#ifndef VB_SPLIT_PREFETCH_PAIR
+#define VB_SPLIT_PREFETCH_PAIR 8  // two frames per thread (unrolled x2), measured: 0 / 4 / 8 / 12 / 16 samples 6.46 / 5.89 / 5.84 / 5.87 / 5.90 ms
+#endif
 #ifndef VB_SPLIT_PREFETCH
 #define VB_SPLIT_PREFETCH 4  // measured: 7.57 -> 7.29 ms per 4000 C2 frames (4 or 8 samples alike)
 #endif
@@ -681,7 +684,7 @@ __global__ void __launch_bounds__(SPLIT ? 128 : 288, SPLIT ? (FPI == 2 ? 2 : kSp
             if (valid) {
                 const int col = a.patch_col[grp.first + p];
                 const float* reg = reinterpret_cast<const float*>(smem + a.off_reg) + d * pitch + col;
-                cross_row_split17<21, float2>(reg, pitch, (int)(reg_slot / 4), a.tmpl + (size_t)(grp.first + p) * P * tp, tp, d,
+                cross_row_split17<21, float2, VB_SPLIT_PREFETCH_PAIR>(reg, pitch, (int)(reg_slot / 4), a.tmpl + (size_t)(grp.first + p) * P * tp, tp, d,
                                       acc, accm);
             } else {
 #pragma unroll
