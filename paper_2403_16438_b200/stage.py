@@ -155,6 +155,17 @@ def preprocess(video, config: StageConfig | None = None, return_corrected: bool 
     followed by summarize(corrected, L, sigma)."""
     v = Video.wrap(video)
     dev = D.require_cuda()
+    if not (isinstance(v.samples, torch.Tensor) and v.samples.is_cuda):
+        # host recording: the C-ABI executor streams it through a two-chunk
+        # device ring (bounded HBM, H2D / compute / D2H overlapped, threaded
+        # host staging); bit-identical to the device-resident path below
+        hs = HostStage(v.height, v.width, config, device=dev.index or 0)
+        try:
+            rec, sp, tp, corr = hs.run(v.samples, corrected=return_corrected)
+        finally:
+            hs.close()
+        out = Video(corr, frame_rate=v.frame_rate) if return_corrected else None
+        return out, M._vectors_from_numpy(rec), [SummaryPair(i, sp[i], tp[i]) for i in range(sp.shape[0])]
     frames = D.as_device_frames(v.samples, dev)
     pre = DevicePreprocessor(v.height, v.width, config)
     try:
