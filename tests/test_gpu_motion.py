@@ -209,3 +209,36 @@ def test_c2_geometry_frame_counts_vs_oracle(cuda, oracle_mod, monkeypatch, n_fra
     np.testing.assert_allclose(sub, ref["sub_conf"][:, :2], atol=1e-3, rtol=0)
     rel = np.abs(corrected.data - ref["corrected"]) / np.maximum(np.abs(ref["corrected"]), 1.0)
     assert rel.max() <= 1e-4
+
+
+@pytest.mark.parametrize("radius", [5, 8])
+def test_high_dynamic_range_vs_oracle(cuda, oracle_mod, monkeypatch, radius):
+    """Full-range uint16 frames (smooth structure spanning ~0..60000 counts,
+    saturated 65535 spots, zero pixels) with sub-pixel drift: the exact integer
+    window statistics (int64 sums of squares near their limits) and the
+    centred float32 cross sums against the float64 oracle."""
+    rng = np.random.default_rng(7)
+    h, w, t = 128, 160, 24
+    yy, xx = np.mgrid[0:h + 20, 0:w + 20].astype(np.float64)
+    scene = 30000 + 25000 * np.sin(yy / 7.0) * np.cos(xx / 9.0) + 4000 * rng.standard_normal((h + 20, w + 20))
+    scene[rng.integers(0, h + 20, 40), rng.integers(0, w + 20, 40)] = 1e9  # saturated spots
+    scene[rng.integers(0, h + 20, 40), rng.integers(0, w + 20, 40)] = -1e9  # zeros
+    frames = np.empty((t, h, w), np.uint16)
+    for i in range(t):
+        dy, dx = rng.uniform(-3, 3, 2)
+        iy, ix = int(np.floor(dy)), int(np.floor(dx))
+        fy, fx = dy - iy, dx - ix
+        y0, x0 = 10 + iy, 10 + ix
+        a = scene[y0:y0 + h, x0:x0 + w]
+        b = scene[y0:y0 + h, x0 + 1:x0 + 1 + w]
+        c = scene[y0 + 1:y0 + 1 + h, x0:x0 + w]
+        d = scene[y0 + 1:y0 + 1 + h, x0 + 1:x0 + 1 + w]
+        f = (1 - fy) * ((1 - fx) * a + fx * b) + fy * ((1 - fx) * c + fx * d)
+        frames[i] = np.clip(np.rint(f + 50 * rng.standard_normal((h, w))), 0, 65535).astype(np.uint16)
+    monkeypatch.setattr(motion, "REFERENCE_FRAMES", 8)
+    corrected, vectors = correct_motion(Video(frames), MotionConfig(search_radius=radius))
+    ref = oracle_mod.preprocess(frames.astype(np.float32), 21, radius, True, 8, 1000)
+    np.testing.assert_array_equal(np.array([[v.dx, v.dy] for v in vectors]), ref["dxdy"])
+    sub = np.array([[v.sub_dx, v.sub_dy] for v in vectors])
+    np.testing.assert_allclose(sub, ref["sub_conf"][:, :2], atol=1e-3, rtol=0)
+    np.testing.assert_allclose([v.confidence for v in vectors], ref["sub_conf"][:, 2], atol=1e-5)
