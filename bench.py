@@ -53,7 +53,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-corrected", action="store_true", help="do not materialise the corrected video")
-    p.add_argument("--cpu-sample", type=int, default=1000, help="frames in the CPU baseline sample")
+    p.add_argument("--cpu-sample", type=int, default=2000, help="frames in the CPU baseline sample (~10 s of CPU work on C2)")
     p.add_argument("--ref-step-frames", type=int, default=400, help="frames per --impl reference step")
     p.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                    help="weak: each rank owns its own T-frame recording shard; strong: one T-frame recording "
