@@ -266,19 +266,30 @@ def correct_motion(video, config: MotionConfig | None = None) -> tuple[Video, li
         raise ValueError("search_radius must be >= 1")
     grid = PatchGrid.cover(v.height, v.width, config.patch_size, margin=config.search_radius)
     dev = D.require_cuda()
-    frames = D.as_device_frames(v.samples, dev)
-    ref = device_reference(frames)
+    samples = v.samples
+    # recordings larger than about a third of the free HBM are processed in
+    # frame chunks (per-frame results do not depend on the chunking)
+    esz = 2 if getattr(samples, "dtype", None) == np.uint16 else 4
+    per_frame = v.height * v.width * (esz + 4)
+    free = torch.cuda.mem_get_info(dev)[0]
+    chunk = v.frames if v.frames * per_frame <= free // 3 else max(1, int(free // 6 // per_frame))
+    m = min(v.frames, REFERENCE_FRAMES)
+    ref = device_reference(D.as_device_frames(samples[:m], dev), m)
     plan = MotionPlan(v.height, v.width, grid.origins, config.patch_size, config.search_radius)
+    out = np.empty((v.frames, v.height, v.width), np.float32)
+    rec = []
     try:
         plan.set_reference(ref)
-        vec, _ = plan.estimate(frames, config.subpixel)
         gain = shading_gain_device(ref, config.shading_sigma) if config.shading_sigma > 0 else None
-        corrected = correct_frames_device(frames, vec, gain)
-        rec = D.motion_to_numpy(vec, v.frames)
-        out = corrected.cpu().numpy()
+        for a in range(0, v.frames, chunk):
+            frames = D.as_device_frames(samples[a:a + chunk], dev)
+            vec, _ = plan.estimate(frames, config.subpixel)
+            out[a:a + frames.shape[0]] = correct_frames_device(frames, vec, gain).cpu().numpy()
+            rec.append(D.motion_to_numpy(vec, frames.shape[0]))
+            del frames, vec
     finally:
         plan.close()
-    return Video(out, frame_rate=v.frame_rate), _vectors_from_numpy(rec)
+    return Video(out, frame_rate=v.frame_rate), _vectors_from_numpy(np.concatenate(rec))
 
 
 def correct_frame(frame: np.ndarray, vector: MotionVector) -> np.ndarray:

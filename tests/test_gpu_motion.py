@@ -5,6 +5,7 @@ import hashlib
 
 import numpy as np
 import pytest
+import torch
 from hypothesis import given, settings
 from hypothesis import strategies as st
 
@@ -242,3 +243,16 @@ def test_high_dynamic_range_vs_oracle(cuda, oracle_mod, monkeypatch, radius):
     sub = np.array([[v.sub_dx, v.sub_dy] for v in vectors])
     np.testing.assert_allclose(sub, ref["sub_conf"][:, :2], atol=1e-3, rtol=0)
     np.testing.assert_allclose([v.confidence for v in vectors], ref["sub_conf"][:, 2], atol=1e-5)
+
+
+def test_correct_motion_chunked_equals_whole(cuda, monkeypatch):
+    """Recordings larger than a third of the free HBM are corrected in frame
+    chunks: identical vectors and frames to the one-shot path."""
+    raw = synth.generate_numpy(synth.CONFIGS["c1"].with_frames(130))
+    monkeypatch.setattr(motion, "REFERENCE_FRAMES", 40)
+    whole, vw = correct_motion(Video(raw), MotionConfig(search_radius=5))
+    per_frame = 128 * 128 * (2 + 4)
+    monkeypatch.setattr(torch.cuda, "mem_get_info", lambda *a: (per_frame * 6 * 37, 1 << 40))  # 37-frame chunks
+    chunked, vc = correct_motion(Video(raw), MotionConfig(search_radius=5))
+    assert vw == vc
+    np.testing.assert_array_equal(whole.data, chunked.data)
