@@ -160,10 +160,25 @@ def summarize(video, segment_length: int = DEFAULT_SEGMENT_LENGTH,
     if segment_length < 2:
         raise ValueError("segment length must be >= 2")
     v = Video.wrap(video)
-    frames = D.as_device_frames(v.samples)
-    sp, tp = summarize_device(frames, segment_length, sigma, highpass_window=highpass_window)
-    sp, tp = sp.cpu().numpy(), tp.cpu().numpy()
-    return [SummaryPair(i, sp[i], tp[i]) for i in range(sp.shape[0])]
+    samples = v.samples
+    esz = 2 if getattr(samples, "dtype", None) == np.uint16 else 4
+    blk_bytes = segment_length * v.height * v.width * esz
+    free = torch.cuda.mem_get_info(D.require_cuda())[0]
+    if highpass_window > 1 or v.frames * v.height * v.width * esz <= free // 3:
+        frames = D.as_device_frames(samples)
+        sp, tp = summarize_device(frames, segment_length, sigma, highpass_window=highpass_window)
+        sp, tp = sp.cpu().numpy(), tp.cpu().numpy()
+        return [SummaryPair(i, sp[i], tp[i]) for i in range(sp.shape[0])]
+    # long recordings: whole blocks per device batch (blocks are independent without the high-pass)
+    if v.frames % segment_length == 1:
+        raise ValueError("temporal summary needs at least 2 frames")
+    per = max(1, int(free // 6 // blk_bytes)) * segment_length
+    pairs = []
+    for a in range(0, v.frames, per):
+        sp, tp = summarize_device(D.as_device_frames(samples[a:a + per]), segment_length, sigma)
+        sp, tp = sp.cpu().numpy(), tp.cpu().numpy()
+        pairs += [SummaryPair(len(pairs) + i, sp[i], tp[i]) for i in range(sp.shape[0])]
+    return pairs
 
 
 def save_summaries(pairs: list[SummaryPair], path: str | Path) -> None:

@@ -184,3 +184,17 @@ class TestSummarize:  # test_summarize.py:150-187
                 checked += 1
                 scored += p.temporal[yy, xx] > np.percentile(p.temporal, 75)
         assert checked > 0 and scored / checked >= 0.6
+
+
+def test_summarize_chunked_equals_whole(cuda, monkeypatch, rng):
+    """Recordings larger than a third of the free HBM are summarised in batches
+    of whole blocks: identical pairs (indices, spatial, temporal)."""
+    v = (rng.random((230, 24, 20), dtype=np.float32) * 1000).astype(np.float32)
+    whole = summarize(Video(v), 50)
+    import torch
+    monkeypatch.setattr(torch.cuda, "mem_get_info", lambda *a: (50 * 24 * 20 * 4 * 6 * 2, 1 << 40))  # 2 blocks per batch
+    chunked = summarize(Video(v), 50)
+    assert [p.segment_index for p in chunked] == [p.segment_index for p in whole] == [0, 1, 2, 3, 4]
+    for p, q in zip(whole, chunked):
+        np.testing.assert_array_equal(p.spatial, q.spatial)
+        np.testing.assert_array_equal(p.temporal, q.temporal)
