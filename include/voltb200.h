@@ -130,6 +130,18 @@ int vb_extract_traces(const float* frames_dev, int64_t n_frames, int height, int
                       const int32_t* roi_ptr_dev, const int32_t* roi_idx_dev, int n_rois, double* out_dev,
                       void* stream);
 
+/* The same traces straight from the RAW frames and their motion vectors
+ * (trace extraction fused with the warp, so the
+ * corrected video is never materialised): the corrected value of each ROI
+ * pixel is interpolated exactly as vb_correct_frames / the stage would
+ * (motion.py:163-200, + the opt-in shading gain, nullable), then averaged like
+ * vb_extract_traces -- bit-identical to it on the corrected video.
+ * frames_dev: uint16 / float32 [n][h][w]; vectors_dev: vb_motion[n] (null =
+ * no motion). */
+int vb_extract_traces_raw(const void* frames_dev, int dtype, const vb_motion* vectors_dev, const float* gain_dev,
+                          int64_t n_frames, int height, int width, const int32_t* roi_ptr_dev,
+                          const int32_t* roi_idx_dev, int n_rois, double* out_dev, void* stream);
+
 /* ---------------- A17 extensions (opt-in, default off) ----------------
  * The north-star's shading/background correction and per-pixel temporal
  * high-pass have NO code in the reference; they

@@ -61,6 +61,7 @@ SIGNATURES = {
     "vb_summarize": (_i32, [_vp, _i32, _vp, _i64, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _vp, _vp]),
     "vb_smooth_frames": (_i32, [_vp, _i32, _i64, _i32, _i32, _vp, _i32, _vp, _vp]),
     "vb_extract_traces": (_i32, [_vp, _i64, _i32, _i32, _vp, _vp, _i32, _vp, _vp]),
+    "vb_extract_traces_raw": (_i32, [_vp, _i32, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _vp, _vp]),
     "vb_summarize_ex": (_i32, [_vp, _i32, _vp, _i64, _i32, _i32, _i32, _vp, _i32, C.POINTER(VbSummaryOpts),
                                _vp, _vp, _vp, _vp]),
     "vb_block_piece": (_i32, [_vp, _i32, _vp, _i64, _i32, _i32, _vp, _i32, _vp, _i64, _i64, _vp, _vp, _vp, _vp]),

@@ -114,6 +114,50 @@ int launch_correct(const void* frames, int dtype, int64_t n, int h, int w, const
     return VB_OK;
 }
 
+// Trace extraction fused with the warp: per (ROI, frame)
+// the corrected samples of the ROI's pixels only are interpolated from the
+// raw frame (warp_sample, + shading gain) and averaged in float64 in
+// traces_kernel's lane order and shuffle tree, so the traces equal those of
+// vb_extract_traces on the corrected video without materialising it.
+__global__ void traces_raw_kernel(const void* __restrict__ frames, int dtype, int64_t n, int h, int w,
+                                  const vb_motion* __restrict__ vec, const float* __restrict__ gain,
+                                  const int32_t* __restrict__ roi_ptr, const int32_t* __restrict__ roi_idx,
+                                  double* __restrict__ out) {
+    const int roi = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int p0 = roi_ptr[roi], p1 = roi_ptr[roi + 1];
+    const double inv_n = 1.0 / (double)(p1 - p0);
+    const int64_t hw = (int64_t)h * w;
+    for (int64_t t = (int64_t)blockIdx.y * nw + warp; t < n; t += (int64_t)gridDim.y * nw) {
+        const WarpOp op = make_warp(vec, t);
+        double s = 0.0;
+        for (int i = p0 + lane; i < p1; i += 32) {
+            const int idx = roi_idx[i], y = idx / w, x = idx - y * w;
+            float v = warp_sample(frames, dtype, t * hw, h, w, op, y, x);
+            if (gain) v = __fdiv_rn(v, __ldg(gain + idx));
+            s += (double)v;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) out[(int64_t)roi * n + t] = s * inv_n;
+    }
+}
+
+int launch_traces_raw(const void* frames, int dtype, int64_t n, int h, int w, const vb_motion* vec,
+                      const float* gain, const int32_t* roi_ptr, const int32_t* roi_idx, int n_rois, double* out,
+                      cudaStream_t s) {
+    if (n <= 0 || n_rois <= 0) return VB_OK;
+    const int threads = 256, warps = threads / 32;
+    const int64_t ychunks = std::min<int64_t>((n + warps - 1) / warps, 65535);
+    dim3 grid((unsigned)n_rois, (unsigned)ychunks);
+    {
+        ProfScope ps(kProfOther, s);
+        traces_raw_kernel<<<grid, threads, 0, s>>>(frames, dtype, n, h, w, vec, gain, roi_ptr, roi_idx, out);
+    }
+    VB_LAUNCHED();
+    return VB_OK;
+}
+
 // ------------------------------------------------------------------ K3
 constexpr int kTY = 32, kTX = 64, kK3Threads = 256;
 constexpr int kMaxWR = 16;

@@ -54,3 +54,15 @@ extern "C" int vb_extract_traces(const float* frames_dev, int64_t n_frames, int 
     return launch_traces(frames_dev, n_frames, (int64_t)height * width, roi_ptr_dev, roi_idx_dev, n_rois, out_dev,
                          (cudaStream_t)stream);
 }
+
+extern "C" int vb_extract_traces_raw(const void* frames_dev, int dtype, const vb_motion* vectors_dev,
+                                     const float* gain_dev, int64_t n_frames, int height, int width,
+                                     const int32_t* roi_ptr_dev, const int32_t* roi_idx_dev, int n_rois,
+                                     double* out_dev, void* stream) {
+    using namespace vb;
+    if (!frames_dev || !roi_ptr_dev || !roi_idx_dev || !out_dev) return fail(VB_EINVAL, "null argument");
+    if (dtype != VB_U16 && dtype != VB_F32) return fail(VB_EINVAL, "unsupported sample type");
+    if (n_rois < 0 || height < 1 || width < 1) return fail(VB_EINVAL, "invalid trace geometry");
+    return launch_traces_raw(frames_dev, dtype, n_frames, height, width, vectors_dev, gain_dev, roi_ptr_dev,
+                             roi_idx_dev, n_rois, out_dev, (cudaStream_t)stream);
+}

@@ -102,6 +102,9 @@ struct SummaryOpts {
 int launch_summarize_ex(const void* frames, int dtype, const vb_motion* vec, int64_t n_avail, int h, int w,
                         int seg_len, const double* weights, int wradius, const SummaryOpts& o, float* corrected,
                         float* spatial, float* temporal, cudaStream_t s);
+int launch_traces_raw(const void* frames, int dtype, int64_t n, int h, int w, const vb_motion* vec,
+                      const float* gain, const int32_t* roi_ptr, const int32_t* roi_idx, int n_rois, double* out,
+                      cudaStream_t s);
 int launch_block_piece(const void* frames, int dtype, const vb_motion* vec, int64_t n, int h, int w,
                        const double* weights, int wradius, const float* gain, int64_t mean_off, int64_t mean_n,
                        float* corrected, float* smoothed, double* partial, cudaStream_t s);

@@ -5,7 +5,9 @@
 ROI mask on the GPU (vb_extract_traces: one warp per (ROI, frame), float64
 accumulation); `dff` and the CSV writer are host bookkeeping like the
 reference.  `extract_traces_device` works on a corrected video already in HBM
-(e.g. DevicePreprocessor's output) without a host round trip.
+(e.g. DevicePreprocessor's output) without a host round trip, and
+`extract_traces_raw_device` on the raw frames + motion vectors, fusing the
+warp so the corrected video is never written.
 """
 from __future__ import annotations
 
@@ -63,6 +65,25 @@ def extract_traces_device(frames_dev: torch.Tensor, masks) -> torch.Tensor:
     out = torch.empty((len(ptr) - 1, t), dtype=torch.float64, device=dev)
     _lib.call("vb_extract_traces", frames_dev.data_ptr(), t, h, w, ptr_d.data_ptr(), idx_d.data_ptr(),
               len(ptr) - 1, out.data_ptr(), D.stream_handle())
+    return out
+
+
+def extract_traces_raw_device(frames_dev: torch.Tensor, vectors_dev: torch.Tensor | None, masks,
+                              gain_dev: torch.Tensor | None = None) -> torch.Tensor:
+    """float64 [K, T] traces straight from the RAW (T, H, W) uint16 / float32
+    frames in HBM and their motion vectors (vb_motion device buffer, e.g.
+    MotionPlan.estimate's output): the corrected video is never materialised
+    (SURVEY 8(f) row 1).  Bit-identical to extract_traces_device on the
+    corrected frames."""
+    t, h, w = frames_dev.shape
+    ptr, idx = _csr(masks, h, w)
+    dev = frames_dev.device
+    ptr_d = torch.from_numpy(ptr).to(dev)
+    idx_d = torch.from_numpy(idx).to(dev)
+    out = torch.empty((len(ptr) - 1, t), dtype=torch.float64, device=dev)
+    _lib.call("vb_extract_traces_raw", frames_dev.data_ptr(), D.vb_dtype(frames_dev), D.ptr(vectors_dev),
+              D.ptr(gain_dev), t, h, w, ptr_d.data_ptr(), idx_d.data_ptr(), len(ptr) - 1, out.data_ptr(),
+              D.stream_handle())
     return out
 
 

@@ -57,3 +57,29 @@ def test_csv(cuda, tmp_path):
     traces.save_traces_csv(trs, tmp_path / "t.csv")
     assert (tmp_path / "t.csv").read_text().splitlines()[1] == "0,1.000000,3.000000"
     assert "500.0" in (tmp_path / "t.json").read_text()
+
+
+@pytest.mark.parametrize("as_u16", [True, False])
+@pytest.mark.parametrize("shading", [0.0, 12.0])
+def test_traces_from_raw_frames_equal_corrected(cuda, as_u16, shading):
+    """vb_extract_traces_raw (warp fused into the trace, no corrected video)
+    == vb_extract_traces on the corrected frames, bit for bit."""
+    from paper_2403_16438_b200 import motion as M
+    cfg = synth.CONFIGS["c1"].with_frames(160)
+    raw, truth = synth.generate_numpy(cfg, return_truth=True)
+    frames = (torch.from_numpy(raw.view(np.int16)).to(cuda).view(torch.uint16) if as_u16
+              else torch.from_numpy(raw.astype(np.float32)).to(cuda))
+    grid = M.PatchGrid.cover(cfg.height, cfg.width, 21, margin=cfg.radius)
+    ref = M.device_reference(frames, 50)
+    plan = M.MotionPlan(cfg.height, cfg.width, grid.origins, 21, cfg.radius)
+    plan.set_reference(ref)
+    vec, _ = plan.estimate(frames, True)
+    gain = M.shading_gain_device(ref, shading) if shading > 0 else None
+    corr = M.correct_frames_device(frames, vec, gain)
+    yy, xx = np.mgrid[:cfg.height, :cfg.width]
+    masks = [((yy - cy) ** 2 + (xx - cx) ** 2) <= 16 for cx, cy in truth.centers]
+    masks.append(np.ones((cfg.height, cfg.width), bool))  # whole frame: edge clamping included
+    want = traces.extract_traces_device(corr, masks).cpu().numpy()
+    got = traces.extract_traces_raw_device(frames, vec, masks, gain).cpu().numpy()
+    np.testing.assert_array_equal(got, want)
+    plan.close()
