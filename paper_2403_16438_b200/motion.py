@@ -9,6 +9,7 @@ host exactly as in the reference.
 from __future__ import annotations
 
 import csv
+import threading
 from dataclasses import dataclass
 from functools import lru_cache
 from pathlib import Path
@@ -219,13 +220,27 @@ def estimate_motion(frame: np.ndarray, reference: np.ndarray, grid: PatchGrid,
     if f.shape != r.shape:
         raise ValueError("frame and reference dimensions differ")
     dev = D.require_cuda()
-    plan = MotionPlan(f.shape[0], f.shape[1], grid.origins, grid.patch_size, search_radius)
-    try:
-        plan.set_reference(D.as_device_frames(r.astype(np.float32, copy=False), dev))
-        vec, _ = plan.estimate(D.as_device_frames(f, dev)[None], subpixel)
-        return _vectors_from_numpy(D.motion_to_numpy(vec, 1))[0]
-    finally:
-        plan.close()
+    # called once per frame with the same grid and reference (like the
+    # reference's motion loop): the calling thread keeps its last plan and
+    # re-prepares the reference only when it changes
+    c = _plan_cache.__dict__
+    origins = np.ascontiguousarray(grid.origins, dtype=np.int32)
+    key = (dev.index, f.shape, origins.tobytes(), grid.patch_size, search_radius)
+    if c.get("key") != key:
+        if c.get("plan") is not None:
+            c["plan"].close()
+        c["plan"] = MotionPlan(f.shape[0], f.shape[1], origins, grid.patch_size, search_radius)
+        c["key"], c["ref"] = key, None
+    plan = c["plan"]
+    r32 = np.ascontiguousarray(r, dtype=np.float32)
+    if c["ref"] is None or not np.array_equal(c["ref"], r32):
+        plan.set_reference(D.as_device_frames(r32, dev))
+        c["ref"] = r32.copy()
+    vec, _ = plan.estimate(D.as_device_frames(f, dev)[None], subpixel)
+    return _vectors_from_numpy(D.motion_to_numpy(vec, 1))[0]
+
+
+_plan_cache = threading.local()
 
 
 def _shift_vectors(n: int, dx: float, dy: float, dev) -> torch.Tensor:
