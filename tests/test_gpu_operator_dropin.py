@@ -46,3 +46,36 @@ def test_reference_correct_motion_with_b200_backend(cuda):
     np.testing.assert_allclose([v.confidence for v in v_b], [v.confidence for v in v_p], atol=1e-6)
     rel = np.abs(c_b - c_p) / np.maximum(np.abs(c_p), 1.0)
     assert rel.max() <= 1e-4
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(not REF.available(), reason="reference not built (oracle/build_ref.sh)")
+def test_reference_correct_motion_throughput_with_b200_backend(cuda):
+    """Timing record (profiles/r01_operator_dropin.json): the reference's own
+    correct_motion on 400 C2 frames with its compiled operator and with ours,
+    1 and all host threads; written to gpurun_out/ when run on the GPU box."""
+    import json
+    import os
+    import time
+    from pathlib import Path
+
+    motion, _s, kernels, video_io = REF.load()
+    cfg = synth.CONFIGS["c2"].with_frames(400)
+    video = video_io.Video(synth.generate_numpy(cfg).astype(np.float32), frame_rate=cfg.fps)
+    old = (kernels.BACKEND, motion.REFERENCE_FRAMES, kernels._native)
+    threads = os.cpu_count() or 1
+    out = {"config": f"c2 400x{cfg.height}x{cfg.width}, r={cfg.radius}: reference correct_motion"}
+    try:
+        motion.REFERENCE_FRAMES = cfg.ref_frames
+        kernels.BACKEND = "native"
+        ours = types.SimpleNamespace(mean_zncc_scores=K.mean_zncc_scores)
+        for name, thr in (("b200", 1), ("b200", threads), ("native", 1), ("native", threads)):
+            kernels._native = ours if name == "b200" else old[2]
+            t0 = time.perf_counter()
+            motion.correct_motion(video, motion.MotionConfig(search_radius=cfg.radius, threads=thr))
+            out[f"{name}_threads{thr}_frames_per_s"] = 400 / (time.perf_counter() - t0)
+    finally:
+        kernels.BACKEND, motion.REFERENCE_FRAMES, kernels._native = old
+    if Path("gpurun_out").is_dir():
+        Path("gpurun_out/operator_dropin.json").write_text(json.dumps(out))
+    assert out["b200_threads1_frames_per_s"] > out["native_threads1_frames_per_s"]
