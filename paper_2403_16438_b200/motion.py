@@ -304,7 +304,7 @@ def correct_motion(video, config: MotionConfig | None = None) -> tuple[Video, li
             del frames, vec
     finally:
         plan.close()
-    return Video(out, frame_rate=v.frame_rate), _vectors_from_numpy(np.concatenate(rec))
+    return Video._trusted(out, frame_rate=v.frame_rate), _vectors_from_numpy(np.concatenate(rec))
 
 
 def correct_frame(frame: np.ndarray, vector: MotionVector) -> np.ndarray:

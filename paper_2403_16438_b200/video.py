@@ -34,6 +34,14 @@ class Video:
         self._data = arr
 
     @classmethod
+    def _trusted(cls, data: np.ndarray, frame_rate: float | None = None) -> "Video":
+        """A float32 (T,H,W) video this package produced (corrected frames:
+        finite and non-negative by construction) -- skips the input scans."""
+        v = cls.__new__(cls)
+        v.frame_rate, v.raw, v._data = frame_rate, None, np.ascontiguousarray(data, dtype=np.float32)
+        return v
+
+    @classmethod
     def wrap(cls, video) -> "Video":
         """Accept this class, voltseg's Video (duck-typed) or an array."""
         if isinstance(video, Video):
