@@ -268,7 +268,9 @@ int vb_stage_set_weights(vb_stage* stage, const double* weights, int wradius);
  * float32 [ceil(n/L)][h][w]; corrected_host: float32 [n][h][w] or NULL;
  * corrected_dev: device float32 [n][h][w] that receives the whole corrected
  * video in HBM, or NULL.  With both NULL the corrected frames are only formed
- * on the fly inside the fused warp/summary kernel. */
+ * on the fly inside the fused warp/summary kernel.  spatial_host and
+ * temporal_host both NULL: motion only (correct_motion, motion.py:217-241) --
+ * vectors and the optional corrected frames, no summaries. */
 int vb_stage_run_host(vb_stage* stage, const void* frames_host, int dtype, int64_t n_frames,
                       vb_motion* vectors_host, float* spatial_host, float* temporal_host,
                       float* corrected_host, float* corrected_dev);

@@ -280,12 +280,16 @@ int vb_stage_run_host_segment(vb_stage* st, const void* frames_host, int dtype, 
 static int stage_run(vb_stage* st, const void* frames_host, int dtype, int64_t n_frames, vb_motion* vectors_host,
                      float* spatial_host, float* temporal_host, float* prob_host, float* corrected_host,
                      float* corrected_dev) {
-    if (!st || !frames_host || !vectors_host || !spatial_host || !temporal_host) return fail(VB_EINVAL, "null argument");
+    if (!st || !frames_host || !vectors_host) return fail(VB_EINVAL, "null argument");
+    // motion only (correct_motion): no summary outputs requested
+    const bool motion_only = !spatial_host && !temporal_host;
+    if (!motion_only && (!spatial_host || !temporal_host)) return fail(VB_EINVAL, "null argument");
+    if (motion_only && prob_host) return fail(VB_EINVAL, "segmentation needs the summaries");
     if (dtype != VB_U16 && dtype != VB_F32) return fail(VB_EINVAL, "unsupported sample type");
     const vb_stage_config& c = st->cfg;
     const int L = c.segment_length;
     if (n_frames < 1) return fail(VB_EINVAL, "video dimensions must all be >= 1");
-    if (n_frames % L == 1) return fail(VB_EINVAL, "temporal summary needs at least 2 frames");
+    if (!motion_only && n_frames % L == 1) return fail(VB_EINVAL, "temporal summary needs at least 2 frames");
     VB_CUDA(cudaSetDevice(c.device));
     const int64_t launches0 = launches().load();
     const size_t hw = (size_t)c.height * c.width;
@@ -304,7 +308,7 @@ static int stage_run(vb_stage* st, const void* frames_host, int dtype, int64_t n
     const bool ring_corr = corrected_host && !corrected_dev;  // corrected chunks need ring buffers
     const bool seg = prob_host != nullptr;
     static const char* cw = getenv("VB_STAGE_CHUNKWISE");  // experiment knob: summaries per chunk
-    const bool piecewise = hh == 0 && !(cw && atoi(cw) == 1);
+    const bool piecewise = !motion_only && hh == 0 && !(cw && atoi(cw) == 1);
     if (st->esz != esz || st->cap < cap || (ring_corr && !st->d_corr[0]) || (corrected_host && !st->h_corr[0]) ||
         (!pinned && !st->h_stage[0]) || (seg && !st->d_prob[0]) || (piecewise && !st->d_smooth)) {
         stage_free_buffers(st);
@@ -415,8 +419,10 @@ static int stage_run(vb_stage* st, const void* frames_host, int dtype, int64_t n
         const int64_t b0 = f0 / L, nb = (nf + L - 1) / L;
         VB_CUDA(cudaEventSynchronize(st->ev_d2h[slot]));
         memcpy(vectors_host + f0, st->h_vec[slot], (size_t)nf * sizeof(vb_motion));
-        memcpy(spatial_host + (size_t)b0 * hw, st->h_sp[slot], (size_t)nb * hw * sizeof(float));
-        memcpy(temporal_host + (size_t)b0 * hw, st->h_tp[slot], (size_t)nb * hw * sizeof(float));
+        if (!motion_only) {
+            memcpy(spatial_host + (size_t)b0 * hw, st->h_sp[slot], (size_t)nb * hw * sizeof(float));
+            memcpy(temporal_host + (size_t)b0 * hw, st->h_tp[slot], (size_t)nb * hw * sizeof(float));
+        }
         if (corrected_host)
             host_copy(corrected_host + (size_t)f0 * hw, st->h_corr[slot], (size_t)nf * hw * sizeof(float));
         if (seg) memcpy(prob_host + (size_t)b0 * hw, st->h_prob[slot], (size_t)nb * hw * sizeof(float));
@@ -449,7 +455,11 @@ static int stage_run(vb_stage* st, const void* frames_host, int dtype, int64_t n
             }
         }
         if (rc) break;
-        if (piecewise) {
+        if (motion_only) {
+            if (corr)
+                rc = launch_correct((const char*)st->d_frames[slot] + (size_t)(f0 - a0) * hw * esz, dtype, nf, c.height,
+                                    c.width, st->d_vec[slot] + (f0 - a0), shade ? st->d_gain : nullptr, corr, st->s_comp);
+        } else if (piecewise) {
             for (int64_t b = 0; b < nb && rc == VB_OK; ++b) {
                 const int cnt = (int)std::min<int64_t>(L, nf - b * L);
                 rc = launch_block_finish(st->d_smooth + (size_t)b * L * hw, 0, 0, cnt, n_frames, 0, (int64_t)hw,
@@ -481,10 +491,12 @@ static int stage_run(vb_stage* st, const void* frames_host, int dtype, int64_t n
         VB_CUDA(cudaStreamWaitEvent(st->s_d2h, st->ev_comp[slot], 0));
         VB_CUDA(cudaMemcpyAsync(st->h_vec[slot], st->d_vec[slot] + (f0 - a0), (size_t)nf * sizeof(vb_motion),
                                 cudaMemcpyDeviceToHost, st->s_d2h));
-        VB_CUDA(cudaMemcpyAsync(st->h_sp[slot], st->d_sp[slot], (size_t)nb * hw * sizeof(float),
-                                cudaMemcpyDeviceToHost, st->s_d2h));
-        VB_CUDA(cudaMemcpyAsync(st->h_tp[slot], st->d_tp[slot], (size_t)nb * hw * sizeof(float),
-                                cudaMemcpyDeviceToHost, st->s_d2h));
+        if (!motion_only) {
+            VB_CUDA(cudaMemcpyAsync(st->h_sp[slot], st->d_sp[slot], (size_t)nb * hw * sizeof(float),
+                                    cudaMemcpyDeviceToHost, st->s_d2h));
+            VB_CUDA(cudaMemcpyAsync(st->h_tp[slot], st->d_tp[slot], (size_t)nb * hw * sizeof(float),
+                                    cudaMemcpyDeviceToHost, st->s_d2h));
+        }
         if (corrected_host)
             VB_CUDA(cudaMemcpyAsync(st->h_corr[slot], corr, (size_t)nf * hw * sizeof(float),
                                     cudaMemcpyDeviceToHost, st->s_d2h));

@@ -104,9 +104,17 @@ __global__ void correct_kernel(const void* __restrict__ frames, int dtype, int64
     }
 }
 
+static int launch_correct_rows(const void* frames, int dtype, int64_t n, int h, int w, const vb_motion* vec,
+                               const float* gain, float* out, cudaStream_t s);
+
+// Corrected frames: the row-strip kernel (correct_rows_kernel below, same
+// arithmetic); correct_kernel stays as the per-pixel restatement
+// (VB_CORRECT_PIXEL=1).
 int launch_correct(const void* frames, int dtype, int64_t n, int h, int w, const vb_motion* vec,
                    const float* gain, float* out, cudaStream_t s) {
     if (n <= 0) return VB_OK;
+    static const bool per_pixel = getenv("VB_CORRECT_PIXEL") != nullptr;  // experiment knob
+    if (!per_pixel) return launch_correct_rows(frames, dtype, n, h, w, vec, gain, out, s);
     const int64_t hw = (int64_t)h * w;
     dim3 grid((unsigned)std::min<int64_t>((hw + 255) / 256, 64), (unsigned)std::min<int64_t>(n, 65535));
     correct_kernel<<<grid, 256, 0, s>>>(frames, dtype, n, h, w, vec, gain, out);
@@ -873,6 +881,27 @@ __global__ void __launch_bounds__(256) correct_rows_kernel(const void* __restric
     }
 }
 
+static int launch_correct_rows(const void* frames, int dtype, int64_t n, int h, int w, const vb_motion* vec,
+                               const float* gain, float* out, cudaStream_t s) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int wq = (w + kCW - 1) / kCW;
+    const int per_frame = ((h + kCR - 1) / kCR) * wq;
+    const int bx = std::max(1, std::min((per_frame + 255) / 256, 64));
+    const int64_t gy = std::min<int64_t>(65535, std::min<int64_t>(n, std::max<int64_t>(1, (int64_t)sms * 8 / bx)));
+    dim3 grid((unsigned)bx, (unsigned)gy);
+    {
+        ProfScope ps(kProfWarpSmooth, s);
+        if (dtype == VB_U16)
+            correct_rows_kernel<true><<<grid, 256, 0, s>>>(frames, n, h, w, vec, gain, out);
+        else
+            correct_rows_kernel<false><<<grid, 256, 0, s>>>(frames, n, h, w, vec, gain, out);
+    }
+    VB_LAUNCHED();
+    return VB_OK;
+}
+
 template <int WR>
 struct K3bGeom {
     static constexpr int EH = kTY + 2 * WR, EW = kTX + 2 * WR, EWP = EW | 1;
@@ -1023,18 +1052,12 @@ static int launch_k3_split(const void* frames, int dtype, const vb_motion* vec, 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     {
-        const int wq = (w + kCW - 1) / kCW;
-        const int per_frame = ((h + kCR - 1) / kCR) * wq;
-        const int bx = std::max(1, std::min((per_frame + 255) / 256, 64));
-        const int64_t gy = std::min<int64_t>(65535, std::min<int64_t>(n, std::max<int64_t>(1, (int64_t)sms * 8 / bx)));
-        dim3 grid((unsigned)bx, (unsigned)gy);
-        ProfScope ps(kProfWarpSmooth, s);
-        if (dtype == VB_U16)
-            correct_rows_kernel<true><<<grid, 256, 0, s>>>(frames, n, h, w, vec, base.gain, corr);
-        else
-            correct_rows_kernel<false><<<grid, 256, 0, s>>>(frames, n, h, w, vec, base.gain, corr);
+        const int rc0 = launch_correct_rows(frames, dtype, n, h, w, vec, base.gain, corr, s);
+        if (rc0) {
+            if (tmp) cudaFreeAsync(tmp, s);
+            return rc0;
+        }
     }
-    VB_LAUNCHED();
     K3Args a = base;
     a.n = n;
     a.smoothed = smoothed;

@@ -279,32 +279,28 @@ def correct_motion(video, config: MotionConfig | None = None) -> tuple[Video, li
     v = Video.wrap(video)
     if config.search_radius < 1:
         raise ValueError("search_radius must be >= 1")
-    grid = PatchGrid.cover(v.height, v.width, config.patch_size, margin=config.search_radius)
+    PatchGrid.cover(v.height, v.width, config.patch_size, margin=config.search_radius)  # geometry errors
     dev = D.require_cuda()
-    samples = v.samples
-    # recordings larger than about a third of the free HBM are processed in
-    # frame chunks (per-frame results do not depend on the chunking)
-    esz = 2 if getattr(samples, "dtype", None) == np.uint16 else 4
-    per_frame = v.height * v.width * (esz + 4)
-    free = torch.cuda.mem_get_info(dev)[0]
-    chunk = v.frames if v.frames * per_frame <= free // 3 else max(1, int(free // 6 // per_frame))
-    m = min(v.frames, REFERENCE_FRAMES)
-    ref = device_reference(D.as_device_frames(samples[:m], dev), m)
-    plan = MotionPlan(v.height, v.width, grid.origins, config.patch_size, config.search_radius)
-    out = np.empty((v.frames, v.height, v.width), np.float32)
-    rec = []
-    try:
-        plan.set_reference(ref)
-        gain = shading_gain_device(ref, config.shading_sigma) if config.shading_sigma > 0 else None
-        for a in range(0, v.frames, chunk):
-            frames = D.as_device_frames(samples[a:a + chunk], dev)
-            vec, _ = plan.estimate(frames, config.subpixel)
-            out[a:a + frames.shape[0]] = correct_frames_device(frames, vec, gain).cpu().numpy()
-            rec.append(D.motion_to_numpy(vec, frames.shape[0]))
-            del frames, vec
-    finally:
-        plan.close()
-    return Video._trusted(out, frame_rate=v.frame_rate), _vectors_from_numpy(np.concatenate(rec))
+    # the host recording streams through the C-ABI executor in motion-only
+    # mode (bounded HBM, H2D / compute / D2H overlapped, threaded staging);
+    # the calling thread keeps the executor for its last geometry
+    from . import stage as S
+
+    sc = S.StageConfig(patch_size=config.patch_size, search_radius=config.search_radius, subpixel=config.subpixel,
+                       ref_frames=REFERENCE_FRAMES, shading_sigma=config.shading_sigma)
+    key = (dev.index or 0, v.height, v.width, repr(sc))
+    c = _stage_cache.__dict__
+    if c.get("key") != key:
+        if c.get("hs") is not None:
+            c["hs"].close()
+        c["hs"], c["key"] = None, None
+        c["hs"] = S.HostStage(v.height, v.width, sc, device=dev.index or 0)
+        c["key"] = key
+    rec, _sp, _tp, out = c["hs"].run(v.samples, corrected=True, summaries=False)
+    return Video._trusted(out, frame_rate=v.frame_rate), _vectors_from_numpy(rec)
+
+
+_stage_cache = threading.local()
 
 
 def correct_frame(frame: np.ndarray, vector: MotionVector) -> np.ndarray:

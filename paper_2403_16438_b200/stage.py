@@ -214,9 +214,10 @@ class HostStage:
             _lib.call("vb_stage_set_shading", self._h, self._sw.ctypes.data, sr)
         self.height, self.width = height, width
 
-    def run(self, frames: np.ndarray, corrected: bool = False):
+    def run(self, frames: np.ndarray, corrected: bool = False, summaries: bool = True):
         """frames: uint16/float32 (T,H,W) host array (pinned or pageable).
-        Returns (vectors record array, spatial [K,H,W], temporal [K,H,W], corrected|None)."""
+        Returns (vectors record array, spatial [K,H,W], temporal [K,H,W], corrected|None);
+        summaries=False: motion only (spatial / temporal are None)."""
         a = frames
         if isinstance(a, torch.Tensor):
             assert not a.is_cuda
@@ -230,8 +231,8 @@ class HostStage:
             ptr, t = a.ctypes.data, a.shape[0]
         k = math.ceil(t / self.cfg.segment_length)
         vec = np.empty(t, dtype=_lib.MOTION_DTYPE)
-        sp = np.empty((k, self.height, self.width), np.float32)
-        tp = np.empty((k, self.height, self.width), np.float32)
+        sp = np.empty((k, self.height, self.width), np.float32) if summaries else None
+        tp = np.empty((k, self.height, self.width), np.float32) if summaries else None
         corr = np.empty((t, self.height, self.width), np.float32) if corrected else None
         self.run_into(ptr, dtype, t, vec, sp, tp, corr)
         return vec, sp, tp, corr

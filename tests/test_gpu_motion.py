@@ -245,14 +245,27 @@ def test_high_dynamic_range_vs_oracle(cuda, oracle_mod, monkeypatch, radius):
     np.testing.assert_allclose([v.confidence for v in vectors], ref["sub_conf"][:, 2], atol=1e-5)
 
 
-def test_correct_motion_chunked_equals_whole(cuda, monkeypatch):
-    """Recordings larger than a third of the free HBM are corrected in frame
-    chunks: identical vectors and frames to the one-shot path."""
+def test_correct_motion_executor_equals_device_pipeline(cuda, monkeypatch):
+    """correct_motion streams host recordings through the C-ABI executor in
+    motion-only mode: identical vectors and frames to the device pipeline
+    (template, MotionPlan.estimate, correct_frames_device), for uint16 and
+    float32 recordings and the opt-in shading gain, across repeated calls."""
     raw = synth.generate_numpy(synth.CONFIGS["c1"].with_frames(130))
     monkeypatch.setattr(motion, "REFERENCE_FRAMES", 40)
-    whole, vw = correct_motion(Video(raw), MotionConfig(search_radius=5))
-    per_frame = 128 * 128 * (2 + 4)
-    monkeypatch.setattr(torch.cuda, "mem_get_info", lambda *a: (per_frame * 6 * 37, 1 << 40))  # 37-frame chunks
-    chunked, vc = correct_motion(Video(raw), MotionConfig(search_radius=5))
-    assert vw == vc
-    np.testing.assert_array_equal(whole.data, chunked.data)
+    for data, shading in ((raw, 0.0), (raw.astype(np.float32), 0.0), (raw, 10.0)):
+        cfg = MotionConfig(search_radius=5, shading_sigma=shading)
+        got, vg = correct_motion(Video(data), cfg)
+        frames = torch.from_numpy(data.view(np.int16) if data.dtype == np.uint16 else data).to(cuda)
+        if data.dtype == np.uint16:
+            frames = frames.view(torch.uint16)
+        ref = motion.device_reference(frames, 40)
+        grid = motion.PatchGrid.cover(128, 128, 21, margin=5)
+        plan = motion.MotionPlan(128, 128, grid.origins, 21, 5)
+        plan.set_reference(ref)
+        vec, _ = plan.estimate(frames, True)
+        gain = motion.shading_gain_device(ref, shading) if shading > 0 else None
+        want = motion.correct_frames_device(frames, vec, gain).cpu().numpy()
+        vw = motion._vectors_from_numpy(motion.D.motion_to_numpy(vec, frames.shape[0]))
+        plan.close()
+        assert vg == vw
+        np.testing.assert_array_equal(got.data, want)
