@@ -269,3 +269,16 @@ def test_correct_motion_executor_equals_device_pipeline(cuda, monkeypatch):
         plan.close()
         assert vg == vw
         np.testing.assert_array_equal(got.data, want)
+
+
+@pytest.mark.parametrize("n", [1, 2, 51, 101])
+def test_correct_motion_any_length(cuda, monkeypatch, n):
+    """correct_motion has no block structure: lengths that leave a one-frame
+    summary block (n % L == 1) are fine in the motion-only executor mode."""
+    raw = synth.generate_numpy(synth.CONFIGS["c1"].with_frames(max(n, 2)))[:n]
+    monkeypatch.setattr(motion, "REFERENCE_FRAMES", 20)
+    corrected, vectors = correct_motion(Video(raw), MotionConfig(search_radius=5))
+    assert corrected.data.shape == raw.shape and len(vectors) == n
+    again, v2 = correct_motion(Video(raw), MotionConfig(search_radius=5))
+    assert v2 == vectors
+    np.testing.assert_array_equal(again.data, corrected.data)
