@@ -19,7 +19,9 @@
 //    sum suffers from (_native_impl.h:18-35).  Each thread owns one (patch,
 //    dy) row of 2R+1 candidates in registers: per template row it loads
 //    S+P-1 frame samples and P template taps (float4 broadcast) and issues
-//    S*P FFMAs.
+//    S*P FFMAs.  At r = 8 (S = 17) a half-warp owns a patch (16 rows + a
+//    shared middle row, cross_row_split17) and each thread carries two
+//    frames through FFMA2 (zncc_group_kernel<21,17,2,true>).
 //  * Per-CTA partial sums of ZNCC over its patches are written in fixed
 //    order (float64) and a finalize kernel sums the groups in fixed order,
 //    divides by N and runs the tie-broken argmax + quadratic fit: fully
