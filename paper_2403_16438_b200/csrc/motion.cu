@@ -612,7 +612,8 @@ __global__ void __launch_bounds__(SPLIT ? 128 : 288, SPLIT ? (FPI == 2 ? 2 : kSp
         }
         // raw boxes -> centred f32 regions: warps over rows, lanes over columns
         // (compile-time-S kernels: threads over (frame, column) units walking
-        // all rows, eight loads in flight, no per-row index arithmetic)
+        // all rows, sixteen loads in flight (measured vs eight: -0.2..0.3 % on
+        // C2/C3/C5), no per-row index arithmetic)
         if (S_CT != 0 && a.dtype == VB_U16 && a.conv_batch >= 2) {
             constexpr int RHC = S_CT != 0 ? P_CT + S_CT - 1 : 1;
             for (int u = tid; u < nf * wu; u += nth) {
@@ -620,13 +621,13 @@ __global__ void __launch_bounds__(SPLIT ? 128 : 288, SPLIT ? (FPI == 2 ? 2 : kSp
                 const uint16_t* raw = reinterpret_cast<const uint16_t*>(smem + f * raw_slot) + boff + c;
                 float* reg = reinterpret_cast<float*>(smem + a.off_reg + f * reg_slot) + c;
 #pragma unroll
-                for (int r0 = 0; r0 < RHC; r0 += 8) {
-                    uint32_t v[8];
+                for (int r0 = 0; r0 < RHC; r0 += 16) {
+                    uint32_t v[16];
 #pragma unroll
-                    for (int k = 0; k < 8; ++k)
+                    for (int k = 0; k < 16; ++k)
                         if (r0 + k < RHC) v[k] = raw[(r0 + k) * a.bw];
 #pragma unroll
-                    for (int k = 0; k < 8; ++k)
+                    for (int k = 0; k < 16; ++k)
                         if (r0 + k < RHC) reg[(r0 + k) * pitch] = u16_minus(v[k], magic);
                 }
             }
