@@ -293,6 +293,16 @@ int vb_stage_run_host_segment(vb_stage* stage, const void* frames_host, int dtyp
                               vb_motion* vectors_host, float* spatial_host, float* temporal_host, float* prob_host,
                               float* corrected_host, float* corrected_dev);
 
+/* Page-locked host memory (cudaHostAlloc, portable).  A corrected_host
+ * buffer passed to vb_stage_run_host that is page-locked (from here or
+ * cudaHostRegister) receives each chunk by a direct device->host copy; a
+ * pageable one goes through the executor's pinned staging slots. */
+int vb_host_alloc(int64_t bytes, void** out);
+int vb_host_free(void* ptr);
+/* memcpy split over n_threads host threads (<= 0: min(8, cores / 2)); the
+ * executor's pageable staging copy (exported for its host-logic tests). */
+int vb_host_copy(void* dst, const void* src, int64_t bytes, int n_threads);
+
 /* Use an externally built template (e.g. all-reduced across ranks) for the
  * following runs instead of averaging the first ref_frames frames of the
  * input (phase A).  ref_dev: device float32 [h][w], copied; NULL restores the

@@ -8,6 +8,7 @@ raised -- never silently routed elsewhere.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
@@ -91,6 +92,9 @@ SIGNATURES = {
     "vb_stage_run_host_segment": (_i32, [_vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "vb_stage_destroy": (_i32, [_vp]),
     "vb_stage_set_reference": (_i32, [_vp, _vp]),
+    "vb_host_alloc": (_i32, [_i64, C.POINTER(_vp)]),
+    "vb_host_free": (_i32, [_vp]),
+    "vb_host_copy": (_i32, [_vp, _vp, _i64, _i32]),
     "vb_launch_count": (_i64, []),
     "vb_prof_enable": (_i32, [_i32]),
     "vb_prof_collect": (_i32, [_vp, _vp, _i32]),
@@ -102,7 +106,8 @@ _lib = None
 
 
 def lib_path() -> Path:
-    return _build.LIB
+    # VB_LIBRARY selects the experiment build (build.py --experiments) for A/B runs
+    return Path(os.environ["VB_LIBRARY"]) if os.environ.get("VB_LIBRARY") else _build.LIB
 
 
 def load(build_if_missing: bool = True) -> C.CDLL:
@@ -111,9 +116,9 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        if build_if_missing:
+        path = lib_path()
+        if build_if_missing and path == _build.LIB:
             _build.build()
-        path = _build.LIB
         if not path.exists():
             raise ImportError(f"{path} is missing; run `python -m paper_2403_16438_b200.build`")
         L = C.CDLL(str(path))

@@ -12,6 +12,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libvoltb200.so"
+LIB_EXP = PKG / "libvoltb200_exp.so"  # experiment build (A/B switches live); loaded only via VB_LIBRARY
 SOURCES = ["capi.cu", "stage.cu", "motion.cu", "summary.cu", "probe.cu", "traces.cu", "unet.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-O3",
@@ -25,18 +26,21 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def _stale() -> bool:
-    if not LIB.exists():
+def _stale(lib: Path = LIB) -> bool:
+    if not lib.exists():
         return True
-    t = LIB.stat().st_mtime
+    t = lib.stat().st_mtime
     deps = [CSRC / s for s in SOURCES] + [CSRC / "vb.cuh", ROOT / "include" / "voltb200.h"]
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
-        return LIB
-    obj_dir = PKG / "build"
+def build(force: bool = False, verbose: bool = False, experiments: bool = False) -> Path:
+    """experiments=True compiles the A/B switches (vb::knob) to read the
+    environment (-DVB_EXPERIMENTS); the product build uses the defaults."""
+    lib = LIB_EXP if experiments else LIB
+    if not force and not _stale(lib):
+        return lib
+    obj_dir = PKG / ("build_exp" if experiments else "build")
     obj_dir.mkdir(exist_ok=True)
     cc = nvcc()
     procs, objs = [], []
@@ -44,6 +48,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         obj = obj_dir / (Path(src).stem + ".o")
         objs.append(obj)
         cmd = [cc, *ARCH, *FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        if experiments:
+            cmd.append("-DVB_EXPERIMENTS")
         if verbose:
             cmd += ["-Xptxas", "-v"]
         procs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
@@ -56,12 +62,11 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             failed.append(src)
     if failed:
         raise RuntimeError(f"nvcc failed for {failed}")
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     subprocess.run([cc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart"], check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, experiments="--experiments" in sys.argv))

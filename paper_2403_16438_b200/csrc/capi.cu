@@ -93,6 +93,8 @@ static int check_origins(int h, int w, const int32_t* origins, int n, int patch,
     if (radius > kMaxRadius) return fail(VB_EINVAL, "search radius too large (max 31)");  // _native.pyx:65-66
     if (radius < 0) return fail(VB_EINVAL, "search_radius must be >= 1");
     if (patch < 1) return fail(VB_EINVAL, "patch size must be >= 1");
+    // exact integer window sums: sum(f - c) in int32 and P^2*sum((f - c)^2) in int64
+    if (patch > kMaxPatch) return fail(VB_EINVAL, "patch size too large (max 180)");
     return VB_OK;
 }
 
@@ -339,9 +341,8 @@ int vb_motion_plan_create(vb_motion_plan** out, int height, int width, int patch
     std::vector<int32_t> col;
     // group width: ~8 patches keeps the CTA at <= ~80 KB of shared memory;
     // shrink the group until the search CTA fits (large radii)
-    static const char* force_g = getenv("VB_GROUP");  // experiment knob: fixed patches per group
-    const int max_g = force_g ? std::max(1, std::min(kMaxGroup, atoi(force_g)))
-                              : choose_group_size(p->origins, patch, radius);
+    const int force_g = knob("VB_GROUP", 0);  // experiment: fixed patches per group
+    const int max_g = force_g > 0 ? std::min(kMaxGroup, force_g) : choose_group_size(p->origins, patch, radius);
     build_groups(p->origins, patch, radius, max_g, groups, col);
     Templates& t = p->t;
     t.n = n_origins;
@@ -351,9 +352,9 @@ int vb_motion_plan_create(vb_motion_plan** out, int height, int width, int patch
         t.max_g = std::max(t.max_g, (int)g.count);
         t.max_wu = std::max(t.max_wu, (int)g.wu);
     }
-    static const char* force_pitch = getenv("VB_PITCH");  // experiment knob (0 = max_wu | 1)
-    t.pitch = force_pitch ? atoi(force_pitch)
-                          : choose_pitch(groups, col, 2 * radius + 1, t.max_wu, patch == 21 && radius == 8);
+    const int force_pitch = knob("VB_PITCH", -1);  // experiment (0 = max_wu | 1)
+    t.pitch = force_pitch >= 0 ? force_pitch
+                               : choose_pitch(groups, col, 2 * radius + 1, t.max_wu, patch == 21 && radius == 8);
     if (t.pitch < t.max_wu) t.pitch = t.max_wu | 1;
     cudaError_t e = cudaSuccess;
     e = e ? e : cudaMalloc(&t.tmpl, (size_t)n_origins * patch * t.tp * sizeof(float));

@@ -273,12 +273,19 @@ __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __gri
             };
             T1 s1 = 0;
             T2 s2 = 0;
+            if constexpr (P_CT != 0) {
 #pragma unroll
-            for (int yy = 0; yy < (P_CT ? P_CT : 64); ++yy) {
-                if (!P_CT && yy >= P) break;
-                const T1 f = sample(yy);
-                s1 += f;
-                s2 += (T2)f * (T2)f;
+                for (int yy = 0; yy < P_CT; ++yy) {
+                    const T1 f = sample(yy);
+                    s1 += f;
+                    s2 += (T2)f * (T2)f;
+                }
+            } else {
+                for (int yy = 0; yy < P; ++yy) {  // any patch size
+                    const T1 f = sample(yy);
+                    s1 += f;
+                    s2 += (T2)f * (T2)f;
+                }
             }
             v1[c] = s1;
             v2[c] = s2;
@@ -320,11 +327,17 @@ __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __gri
             const T2* r2 = v2 + dy * vp + col;
             T1 h1 = 0;
             T2 h2 = 0;
+            if constexpr (P_CT != 0) {
 #pragma unroll
-            for (int xx = 0; xx < (P_CT ? P_CT : 64); ++xx) {
-                if (!P_CT && xx >= P) break;
-                h1 += r1[xx];
-                h2 += r2[xx];
+                for (int xx = 0; xx < P_CT; ++xx) {
+                    h1 += r1[xx];
+                    h2 += r2[xx];
+                }
+            } else {
+                for (int xx = 0; xx < P; ++xx) {  // any patch size
+                    h1 += r1[xx];
+                    h2 += r2[xx];
+                }
             }
             float* out = a.inv + ((size_t)t * a.n_patches + gp) * a.ss_pad + (size_t)dy * S;
             float ivs[S_CT ? S_CT : 1];
@@ -334,10 +347,14 @@ __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __gri
                 float iv = 0.0f;
                 if constexpr (INT) {
                     // n*fvar exactly; 1/sqrt(fvar*rv) = P / sqrt(n*fvar*rv).  int64 -> f64 by
-                    // the 2^52 bit trick (exact below 2^52) instead of the conversion unit.
+                    // the 2^52 bit trick (exact below 2^52, i.e. always for P <= 45 on u16
+                    // data) instead of the conversion unit; larger values convert (rounded,
+                    // like the reference's float64 sums).
                     const long long nf = (long long)P * P * h2 - (long long)h1 * h1;
                     if (rv > 0.0 && nf > 0) {
-                        const double nfd = __longlong_as_double(0x4330000000000000LL | nf) - 4503599627370496.0;
+                        const double nfd = nf < (1LL << 52)
+                                               ? __longlong_as_double(0x4330000000000000LL | nf) - 4503599627370496.0
+                                               : (double)nf;
                         iv = (float)((double)P * (kFastRsqrt ? rsqrt_pos(nfd * rv) : rsqrt(nfd * rv)));
                     }
                 } else {
@@ -985,17 +1002,15 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
         if (e2 > e1 + 0.15 && zncc_smem(patch, radius, t.max_g, t.max_wu, dtype, 2, true, t.pitch).total <= 112 * 1024)
             fpi = 2;
     }
-    static const char* force_fpi = getenv("VB_FPI");  // experiment knob
-    if (fast && force_fpi && (atoi(force_fpi) == 1 || atoi(force_fpi) == 2)) fpi = atoi(force_fpi);
+    const int force_fpi = knob("VB_FPI", 0);  // experiment
+    if (fast && (force_fpi == 1 || force_fpi == 2)) fpi = force_fpi;
     // S = 17: half-warp per patch with the shared middle row (cross_row_split17)
-    static const char* no_split = getenv("VB_NO_SPLIT");  // experiment knob
-    bool split = fast && patch == 21 && S == 17 && fpi == 1 && !no_split;
+    bool split = fast && patch == 21 && S == 17 && fpi == 1 && !knob("VB_NO_SPLIT", 0);
     // paired split kernel: each thread carries two frames through FFMA2 (half the FMA
     // instructions, 226 registers, twice the shared memory per CTA: 2 CTAs per SM).
     // Measured on C2: 6.62 -> 6.54 ms per 4000 frames; the issue rate drops from 82 % to
     // 51 % and the FMA pipe (2 cycles per FFMA2) becomes the limiter inside the cross phase
-    static const char* pair_env = getenv("VB_SPLIT_PAIR");  // experiment knob: 0 off, 1 on
-    const bool pair = split && (pair_env ? atoi(pair_env) == 1 : true) &&
+    const bool pair = split && knob("VB_SPLIT_PAIR", 1) == 1 &&
                       zncc_smem(patch, radius, t.max_g, t.max_wu, dtype, 2, true, t.pitch).total +
                               2 * (size_t)t.max_g * ((S * S + 3) & ~3) * 4 <= 112 * 1024;
     if (pair) fpi = 2;
@@ -1006,8 +1021,7 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     void (*stats_fn)(ZnccArgs, CUtensorMap) =
         patch == 21 ? (dtype == VB_U16 ? zncc_stats_kernel<true, 21> : zncc_stats_kernel<false, 21>)
                     : (dtype == VB_U16 ? zncc_stats_kernel<true, 0> : zncc_stats_kernel<false, 0>);
-    static const bool no_stats_s = getenv("VB_NO_STATS_S") != nullptr;  // experiment knob
-    if (patch == 21 && dtype == VB_U16 && !no_stats_s) {  // compile-time S: unrolled horizontal chains
+    if (patch == 21 && dtype == VB_U16 && !knob("VB_NO_STATS_S", 0)) {  // compile-time S: unrolled horizontal chains
         if (S == 17) stats_fn = zncc_stats_kernel<true, 21, 17>;
         if (S == 21) stats_fn = zncc_stats_kernel<true, 21, 21>;
         if (S == 25) stats_fn = zncc_stats_kernel<true, 21, 25>;
@@ -1020,9 +1034,8 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     const int ss_pad_ = (S * S + 3) & ~3;
     // measured on C2 (split kernel): 7.05 -> 6.78 ms with the conversion batching; kept to the
     // split kernel -- the extra registers cost the generic S != 17 kernels a resident CTA
-    static const char* inv_mode = getenv("VB_INV_SMEM");  // experiment knob: 0 off
-    const bool want_inv = fast && (fpi == 1 || pair) && !(inv_mode && atoi(inv_mode) == 0) &&
-                          (patch == 21 && S == 17 || (inv_mode && atoi(inv_mode) == 1));
+    const int inv_mode = knob("VB_INV_SMEM", -1);  // experiment: 0 off, 1 all kernels
+    const bool want_inv = fast && (fpi == 1 || pair) && inv_mode != 0 && ((patch == 21 && S == 17) || inv_mode == 1);
     const size_t inv_buf = want_inv ? (size_t)fpi * t.max_g * ss_pad_ * sizeof(float) : 0;
     const size_t search_smem = ((sp.total + 15) & ~(size_t)15) + inv_buf;
     if (search_smem > 227 * 1024) return fail(VB_EINVAL, "patch group does not fit in shared memory");
@@ -1040,10 +1053,9 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     a.nch = fast ? 1 : (S + kGenericDXB - 1) / kGenericDXB;
     a.ss_pad = ss_pad_;
     a.off_inv = -1;
-    static const char* cb = getenv("VB_CONV_BATCH");  // experiment knob
     // 2: compile-time-S kernels convert column-major (measured per search: C2 6.90 -> 6.62 ms per
     // 4000 frames, C3 14.74 -> 13.55 ms per 2000, C5 20.91 -> 19.81 ms per 1000)
-    a.conv_batch = cb ? atoi(cb) : 2;
+    a.conv_batch = knob("VB_CONV_BATCH", 2);
     a.pitch_cap = sp.pitch;
     a.bw = sp.bw;
     a.bh = sp.bh;
@@ -1058,8 +1070,7 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     // one tensor map over the whole launch range (frames as the z dimension)
     CUtensorMap tmap;
     memset(&tmap, 0, sizeof(tmap));
-    static const bool no_tma = getenv("VB_NO_TMA") != nullptr;  // debug toggle: plain-load staging
-    a.use_tma = !no_tma && make_frames_tmap(&tmap, frames, dtype, n_frames, h, w, sp.bhc, sp.bw) ? 1 : 0;
+    a.use_tma = !knob("VB_NO_TMA", 0) && make_frames_tmap(&tmap, frames, dtype, n_frames, h, w, sp.bhc, sp.bw) ? 1 : 0;
 
     a.rows = split ? 16 : S;
     const int items = (pair ? 1 : fpi) * t.max_g * a.rows * nch;
@@ -1073,8 +1084,8 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     const size_t per_frame_part = (size_t)t.n_groups * SS * sizeof(double);
     const size_t per_frame_inv = (size_t)t.n * a.ss_pad * sizeof(float);
     int64_t batch = std::max<int64_t>(1, (int64_t)(((size_t)1 << 30) / (per_frame_part + per_frame_inv)));
-    static const char* force_batch = getenv("VB_ZNCC_BATCH");  // experiment knob (frames per stats+search pair)
-    if (force_batch && atoll(force_batch) > 0) batch = atoll(force_batch);
+    const int force_batch = knob("VB_ZNCC_BATCH", 0);  // experiment: frames per stats+search pair
+    if (force_batch > 0) batch = force_batch;
     batch = std::min(batch, n_frames);
     double* partial = nullptr;
     float* inv = nullptr;

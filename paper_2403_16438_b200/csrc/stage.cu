@@ -25,29 +25,36 @@ using namespace vb;
 // one thread moves ~10-14 GB/s, below the ~55 GB/s PCIe stream it feeds, so
 // large copies are split over a few threads (measured on C2 from a plain
 // numpy recording: 53 k frames/s with one thread).
-static void host_copy(void* dst, const void* src, size_t bytes) {
+static int host_copy_threads() {
     static const int nthr = [] {
-        const char* e = getenv("VB_HOST_COPY_THREADS");  // experiment knob
-        if (e && atoi(e) > 0) return atoi(e);
         const unsigned hc = std::thread::hardware_concurrency();
         return (int)std::max(1u, std::min(8u, hc ? hc / 2 : 1u));
     }();
+    return nthr;
+}
+
+// Split [0, bytes) into nt contiguous ranges with 64-byte aligned interior
+// boundaries; range i = [i*step, min(bytes, (i+1)*step)) and the last one
+// always ends at `bytes` (step = ceil(bytes / nt) rounded up to 64).
+static void host_copy_n(void* dst, const void* src, size_t bytes, int nthr) {
     constexpr size_t kMinPerThread = 4u << 20;
-    const int nt = (int)std::min<size_t>((size_t)nthr, std::max<size_t>(1, bytes / kMinPerThread));
+    const int nt = (int)std::min<size_t>((size_t)std::max(1, nthr), std::max<size_t>(1, bytes / kMinPerThread));
     if (nt <= 1) {
         memcpy(dst, src, bytes);
         return;
     }
-    const size_t step = (bytes / nt + 63) & ~(size_t)63;
+    const size_t step = ((bytes + nt - 1) / nt + 63) & ~(size_t)63;
     std::vector<std::thread> pool;
     pool.reserve(nt - 1);
     for (int i = 1; i < nt; ++i) {
-        const size_t o = std::min(bytes, i * step), e = std::min(bytes, o + step);
+        const size_t o = std::min(bytes, i * step), e = (i == nt - 1) ? bytes : std::min(bytes, o + step);
         if (e > o) pool.emplace_back([=] { memcpy((char*)dst + o, (const char*)src + o, e - o); });
     }
     memcpy(dst, src, std::min(bytes, step));
     for (auto& th : pool) th.join();
 }
+
+static void host_copy(void* dst, const void* src, size_t bytes) { host_copy_n(dst, src, bytes, host_copy_threads()); }
 
 struct vb_stage {
     vb_stage_config cfg{};
@@ -159,15 +166,28 @@ int vb_stage_create(vb_stage** out, const vb_stage_config* cfg) {
         delete st;
         return rc;
     }
-    // scipy _gaussian_kernel1d(sigma, 0, ceil(3 sigma)) (summarize.py:71).
-    // NOTE: libm exp may differ from numpy's in the last ulp; the Python layer
-    // passes numpy-computed weights to vb_summarize for bit-exact parity.
+    // scipy _gaussian_kernel1d(sigma, 0, ceil(3 sigma)) (summarize.py:71),
+    // normalised by numpy's pairwise sum (eight accumulators, combined as
+    // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the tail in order).  For the
+    // default sigma = 3 libm's exp equals numpy's and the taps are bit-identical
+    // to scipy's; for other sigmas numpy's exp may differ in the last ulp, so
+    // vb_stage_set_weights with numpy-computed taps is the parity path.
     st->wradius = (int)ceil(3.0 * cfg->sigma);
-    st->weights.resize(2 * st->wradius + 1);
-    double tot = 0.0;
-    for (int i = -st->wradius; i <= st->wradius; ++i) {
+    const int nw = 2 * st->wradius + 1;
+    st->weights.resize(nw);
+    for (int i = -st->wradius; i <= st->wradius; ++i)
         st->weights[i + st->wradius] = exp(-0.5 / (cfg->sigma * cfg->sigma) * (double)(i * i));
-        tot += st->weights[i + st->wradius];
+    double tot = 0.0;
+    if (nw < 8) {
+        for (int i = 0; i < nw; ++i) tot += st->weights[i];
+    } else {
+        double r[8];
+        for (int j = 0; j < 8; ++j) r[j] = st->weights[j];
+        int i = 8;
+        for (; i < nw - nw % 8; i += 8)
+            for (int j = 0; j < 8; ++j) r[j] += st->weights[i + j];
+        tot = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < nw; ++i) tot += st->weights[i];
     }
     for (auto& wv : st->weights) wv /= tot;
     const int L = cfg->segment_length;
@@ -277,10 +297,39 @@ int vb_stage_run_host_segment(vb_stage* st, const void* frames_host, int dtype, 
                      corrected_host, corrected_dev);
 }
 
+static int stage_run_impl(vb_stage* st, const void* frames_host, int dtype, int64_t n_frames,
+                          vb_motion* vectors_host, float* spatial_host, float* temporal_host, float* prob_host,
+                          float* corrected_host, float* corrected_dev);
+
+// Every exit (including errors part-way through the chunk loop) synchronises
+// all stage streams, so no copy still reads the caller's frames or writes its
+// outputs after the call returns.
+static int stage_sync_all(vb_stage* st) {
+    cudaError_t e = cudaSuccess;
+    for (cudaStream_t s : {st->s_h2d, st->s_comp, st->s_d2h, st->s_seg}) {
+        if (!s) continue;
+        const cudaError_t es = cudaStreamSynchronize(s);
+        if (e == cudaSuccess) e = es;
+    }
+    return e;
+}
+
 static int stage_run(vb_stage* st, const void* frames_host, int dtype, int64_t n_frames, vb_motion* vectors_host,
                      float* spatial_host, float* temporal_host, float* prob_host, float* corrected_host,
                      float* corrected_dev) {
     if (!st || !frames_host || !vectors_host) return fail(VB_EINVAL, "null argument");
+    const int64_t launches0 = launches().load();
+    int rc = stage_run_impl(st, frames_host, dtype, n_frames, vectors_host, spatial_host, temporal_host, prob_host,
+                            corrected_host, corrected_dev);
+    const cudaError_t e = (cudaError_t)stage_sync_all(st);
+    if (rc == VB_OK && e != cudaSuccess) rc = cuda_fail(e, "vb_stage_run_host");
+    st->last_launches = launches().load() - launches0;
+    return rc;
+}
+
+static int stage_run_impl(vb_stage* st, const void* frames_host, int dtype, int64_t n_frames,
+                          vb_motion* vectors_host, float* spatial_host, float* temporal_host, float* prob_host,
+                          float* corrected_host, float* corrected_dev) {
     // motion only (correct_motion): no summary outputs requested
     const bool motion_only = !spatial_host && !temporal_host;
     if (!motion_only && (!spatial_host || !temporal_host)) return fail(VB_EINVAL, "null argument");
@@ -291,7 +340,6 @@ static int stage_run(vb_stage* st, const void* frames_host, int dtype, int64_t n
     if (n_frames < 1) return fail(VB_EINVAL, "video dimensions must all be >= 1");
     if (!motion_only && n_frames % L == 1) return fail(VB_EINVAL, "temporal summary needs at least 2 frames");
     VB_CUDA(cudaSetDevice(c.device));
-    const int64_t launches0 = launches().load();
     const size_t hw = (size_t)c.height * c.width;
     const size_t esz = dtype == VB_U16 ? 2 : 4;
     const int64_t C = st->chunk;
@@ -300,16 +348,23 @@ static int stage_run(vb_stage* st, const void* frames_host, int dtype, int64_t n
     const int64_t cap = C + 2 * hh;
     const bool shade = !st->shade_w.empty();
 
-    cudaPointerAttributes attr;
-    bool pinned = cudaPointerGetAttributes(&attr, frames_host) == cudaSuccess && attr.type == cudaMemoryTypeHost;
-    cudaGetLastError();
+    auto is_pinned = [](const void* p) {
+        cudaPointerAttributes attr;
+        const bool r = p && cudaPointerGetAttributes(&attr, p) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+        return r;
+    };
+    const bool pinned = is_pinned(frames_host);
+    // page-locked corrected output (cudaHostAlloc / cudaHostRegister): chunks
+    // are copied device->host straight into it, no staging slot or host copy
+    const bool corr_direct = corrected_host && is_pinned(corrected_host) &&
+                             is_pinned((const char*)corrected_host + (size_t)n_frames * hw * sizeof(float) - 1);
 
     // (re)allocate the two-slot ring
     const bool ring_corr = corrected_host && !corrected_dev;  // corrected chunks need ring buffers
     const bool seg = prob_host != nullptr;
-    static const char* cw = getenv("VB_STAGE_CHUNKWISE");  // experiment knob: summaries per chunk
-    const bool piecewise = !motion_only && hh == 0 && !(cw && atoi(cw) == 1);
-    if (st->esz != esz || st->cap < cap || (ring_corr && !st->d_corr[0]) || (corrected_host && !st->h_corr[0]) ||
+    const bool piecewise = !motion_only && hh == 0 && knob("VB_STAGE_CHUNKWISE", 0) != 1;
+    if (st->esz != esz || st->cap < cap || (ring_corr && !st->d_corr[0]) || (corrected_host && !corr_direct && !st->h_corr[0]) ||
         (!pinned && !st->h_stage[0]) || (seg && !st->d_prob[0]) || (piecewise && !st->d_smooth)) {
         stage_free_buffers(st);
         cudaError_t e = cudaSuccess;
@@ -322,7 +377,7 @@ static int stage_run(vb_stage* st, const void* frames_host, int dtype, int64_t n
             e = e ? e : cudaHostAlloc(&st->h_vec[i], (size_t)C * sizeof(vb_motion), cudaHostAllocDefault);
             e = e ? e : cudaHostAlloc(&st->h_sp[i], (size_t)cblk * hw * sizeof(float), cudaHostAllocDefault);
             e = e ? e : cudaHostAlloc(&st->h_tp[i], (size_t)cblk * hw * sizeof(float), cudaHostAllocDefault);
-            if (corrected_host)
+            if (corrected_host && !corr_direct)
                 e = e ? e : cudaHostAlloc(&st->h_corr[i], (size_t)C * hw * sizeof(float), cudaHostAllocDefault);
             if (!pinned) e = e ? e : cudaHostAlloc(&st->h_stage[i], (size_t)cap * hw * esz, cudaHostAllocDefault);
             if (seg) {
@@ -423,7 +478,7 @@ static int stage_run(vb_stage* st, const void* frames_host, int dtype, int64_t n
             memcpy(spatial_host + (size_t)b0 * hw, st->h_sp[slot], (size_t)nb * hw * sizeof(float));
             memcpy(temporal_host + (size_t)b0 * hw, st->h_tp[slot], (size_t)nb * hw * sizeof(float));
         }
-        if (corrected_host)
+        if (corrected_host && !corr_direct)
             host_copy(corrected_host + (size_t)f0 * hw, st->h_corr[slot], (size_t)nf * hw * sizeof(float));
         if (seg) memcpy(prob_host + (size_t)b0 * hw, st->h_prob[slot], (size_t)nb * hw * sizeof(float));
         return VB_OK;
@@ -498,8 +553,8 @@ static int stage_run(vb_stage* st, const void* frames_host, int dtype, int64_t n
                                     cudaMemcpyDeviceToHost, st->s_d2h));
         }
         if (corrected_host)
-            VB_CUDA(cudaMemcpyAsync(st->h_corr[slot], corr, (size_t)nf * hw * sizeof(float),
-                                    cudaMemcpyDeviceToHost, st->s_d2h));
+            VB_CUDA(cudaMemcpyAsync(corr_direct ? corrected_host + (size_t)f0 * hw : st->h_corr[slot], corr,
+                                    (size_t)nf * hw * sizeof(float), cudaMemcpyDeviceToHost, st->s_d2h));
         if (seg)
             VB_CUDA(cudaMemcpyAsync(st->h_prob[slot], st->d_prob[slot], (size_t)nb * hw * sizeof(float),
                                     cudaMemcpyDeviceToHost, st->s_d2h));
@@ -516,21 +571,13 @@ static int stage_run(vb_stage* st, const void* frames_host, int dtype, int64_t n
         if (k >= 1) rc = drain(k - 1);
     }
     if (rc == VB_OK && nchunks >= 1) rc = drain(nchunks - 1);
-    cudaError_t e1 = cudaStreamSynchronize(st->s_h2d);
-    cudaError_t e2 = cudaStreamSynchronize(st->s_comp);
-    cudaError_t e3 = cudaStreamSynchronize(st->s_d2h);
-    cudaError_t e4 = st->s_seg ? cudaStreamSynchronize(st->s_seg) : cudaSuccess;
-    if (rc == VB_OK) {
-        cudaError_t e = e1 ? e1 : (e2 ? e2 : (e3 ? e3 : e4));
-        if (e != cudaSuccess) rc = cuda_fail(e, "vb_stage_run_host");
-    }
-    st->last_launches = launches().load() - launches0;
     return rc;
 }
 
 int vb_stage_destroy(vb_stage* st) {
     if (!st) return VB_OK;
-    if (st->s_comp) cudaStreamSynchronize(st->s_comp);
+    cudaSetDevice(st->cfg.device);
+    stage_sync_all(st);
     stage_free_buffers(st);
     vb_motion_plan_destroy(st->plan);
     cudaFree(st->d_tsum);
@@ -546,13 +593,34 @@ int vb_stage_destroy(vb_stage* st) {
     if (st->s_comp) cudaStreamDestroy(st->s_comp);
     if (st->s_h2d) cudaStreamDestroy(st->s_h2d);
     if (st->s_d2h) cudaStreamDestroy(st->s_d2h);
-    if (st->s_seg) {
-        cudaStreamSynchronize(st->s_seg);
-        cudaStreamDestroy(st->s_seg);
-    }
+    if (st->s_seg) cudaStreamDestroy(st->s_seg);
     for (int i = 0; i < 2; ++i)
         if (st->ev_seg[i]) cudaEventDestroy(st->ev_seg[i]);
     delete st;
+    return VB_OK;
+}
+
+int vb_host_alloc(int64_t bytes, void** out) {
+    if (!out || bytes < 0) return fail(VB_EINVAL, "null argument");
+    *out = nullptr;
+    if (bytes == 0) return VB_OK;
+    const cudaError_t e = cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *out = nullptr;
+        return fail(VB_ENOMEM, std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+    }
+    return VB_OK;
+}
+
+int vb_host_free(void* p) {
+    if (p) VB_CUDA(cudaFreeHost(p));
+    return VB_OK;
+}
+
+int vb_host_copy(void* dst, const void* src, int64_t bytes, int n_threads) {
+    if ((!dst || !src) && bytes > 0) return fail(VB_EINVAL, "null argument");
+    if (bytes > 0) host_copy_n(dst, src, (size_t)bytes, n_threads > 0 ? n_threads : host_copy_threads());
     return VB_OK;
 }
 

@@ -88,38 +88,15 @@ __device__ __forceinline__ float warp_sample(const void* f, int dtype, int64_t b
     return __fadd_rn(__fmul_rn(op.omy, top), __fmul_rn(op.fy, bot));
 }
 
-// gain (A17 shading correction, opt-in): corrected = warped / gain[y][x]
-// (IEEE float32 division); null = off.
-__global__ void correct_kernel(const void* __restrict__ frames, int dtype, int64_t n, int h, int w,
-                               const vb_motion* __restrict__ vec, const float* __restrict__ gain,
-                               float* __restrict__ out) {
-    const int64_t hw = (int64_t)h * w;
-    for (int64_t t = blockIdx.y; t < n; t += gridDim.y) {
-        const WarpOp op = make_warp(vec, t);
-        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hw; i += (int64_t)gridDim.x * blockDim.x) {
-            const int y = (int)(i / w), x = (int)(i - (int64_t)y * w);
-            const float v = warp_sample(frames, dtype, t * hw, h, w, op, y, x);
-            out[t * hw + i] = gain ? __fdiv_rn(v, __ldg(gain + i)) : v;
-        }
-    }
-}
-
 static int launch_correct_rows(const void* frames, int dtype, int64_t n, int h, int w, const vb_motion* vec,
                                const float* gain, float* out, cudaStream_t s);
 
-// Corrected frames: the row-strip kernel (correct_rows_kernel below, same
-// arithmetic); correct_kernel stays as the per-pixel restatement
-// (VB_CORRECT_PIXEL=1).
+// Corrected frames (translate, motion.py:163-200; + A17 gain, opt-in):
+// the row-strip kernel correct_rows_kernel below.
 int launch_correct(const void* frames, int dtype, int64_t n, int h, int w, const vb_motion* vec,
                    const float* gain, float* out, cudaStream_t s) {
     if (n <= 0) return VB_OK;
-    static const bool per_pixel = getenv("VB_CORRECT_PIXEL") != nullptr;  // experiment knob
-    if (!per_pixel) return launch_correct_rows(frames, dtype, n, h, w, vec, gain, out, s);
-    const int64_t hw = (int64_t)h * w;
-    dim3 grid((unsigned)std::min<int64_t>((hw + 255) / 256, 64), (unsigned)std::min<int64_t>(n, 65535));
-    correct_kernel<<<grid, 256, 0, s>>>(frames, dtype, n, h, w, vec, gain, out);
-    VB_LAUNCHED();
-    return VB_OK;
+    return launch_correct_rows(frames, dtype, n, h, w, vec, gain, out, s);
 }
 
 // Trace extraction fused with the warp: per (ROI, frame)
@@ -357,173 +334,11 @@ __device__ __forceinline__ void src_span(int lo, int hi, int n, int i0, int& a0,
     a1 = clampi(mx - i0, 0, n - 1);
 }
 
-// K3 with compile-time tile geometry and a TMA-prefetched raw box: one CTA
-// per (tile, frame slice), persistent over frames z, z+gz, ...  The elected
-// thread issues the next frame's box (16-byte aligned start, zero-filled out
-// of bounds) as soon as the current box has been consumed, so the global
-// latency overlaps the two float64 passes.
-template <int WR, bool U16, bool SHADE>
-__global__ void __launch_bounds__(kK3Threads, 3) warp_smooth_tma_kernel(K3Args a, const __grid_constant__ CUtensorMap tmap) {
-    constexpr int EH = kTY + 2 * WR, EW = kTX + 2 * WR, EWP = EW | 1;
-    constexpr int ALN = U16 ? 8 : 4;                                   // 16-byte alignment in samples
-    constexpr int BWB = ((EW + 1 + ALN - 1 + ALN - 1) / ALN) * ALN;    // box width
-    constexpr int BHB = EH + 1;                                        // box height
-    using S_T = typename std::conditional<U16, uint16_t, float>::type;
-    extern __shared__ __align__(128) unsigned char smem[];
-    S_T* sRaw = reinterpret_cast<S_T*>(smem);                                          // [BHB][BWB]
-    double* sC = reinterpret_cast<double*>(smem + (((size_t)BHB * BWB * sizeof(S_T) + 127) & ~(size_t)127));  // [EH][EWP]
-    double* sV = sC + (size_t)EH * EWP;                                                // [kTY][EWP]
-    __shared__ double s_w[WR + 1];
-    __shared__ int s_ra[EH], s_rc[EH], s_xa[EW], s_xb[EW];
-    __shared__ int s_gy[SHADE ? EH : 1], s_gx[SHADE ? EW : 1];  // reflected output coordinates (gain lookups)
-    __shared__ int s_box[2];
-    __shared__ __align__(8) uint64_t bar;
-    const int tid = threadIdx.x;
-    if (tid <= WR) s_w[tid] = a.wt.w[WR - tid];  // s_w[k] = weight at offset -k (symmetric)
-    const int ty0 = blockIdx.y * kTY, tx0 = blockIdx.x * kTX;
-    const int64_t hw = (int64_t)a.h * a.w;
-    if (tid == 0) {
-        mbar_init(&bar, 1);
-        fence_mbar_init();
-        tma_prefetch_desc(&tmap);
-    }
-    __syncthreads();
-    // elected thread: issue frame t's box; returns its origin via s_box
-    auto issue = [&](int64_t t) {
-        const WarpOp op = make_warp(a.vec, t);
-        int y0, y1, x0, x1;
-        src_span(ty0 - WR, ty0 + kTY + WR, a.h, op.iy, y0, y1);
-        src_span(tx0 - WR, tx0 + kTX + WR, a.w, op.ix, x0, x1);
-        const int x0a = x0 & ~(ALN - 1);
-        mbar_expect_tx(&bar, (uint32_t)(BWB * BHB * sizeof(S_T)));
-        tma_load_3d(sRaw, &tmap, x0a, y0, (int)t, &bar);
-        return make_int2(x0a, y0);
-    };
-    int2 origin_next = make_int2(0, 0);
-    int64_t t = blockIdx.z;
-    if (tid == 0 && t < a.n) origin_next = issue(t);
-    uint32_t phase = 0;
-    const double* wk = s_w;  // wk[k] = w(-k)
-    for (; t < a.n; t += gridDim.z) {
-        const WarpOp op = make_warp(a.vec, t);
-        if (tid == 0) {
-            s_box[0] = origin_next.x;
-            s_box[1] = origin_next.y;
-        }
-        // 1. index tables (all threads; the box origin is published with them)
-        for (int i = tid; i < EH + EW; i += kK3Threads) {
-            if (i < EH) {
-                const int y = reflect_index(ty0 - WR + i, a.h);
-                if constexpr (SHADE) s_gy[i] = y;
-                s_ra[i] = clampi(y - op.iy, 0, a.h - 1);
-                s_rc[i] = clampi(y - op.iy - 1, 0, a.h - 1);
-            } else {
-                const int e = i - EH;
-                const int x = reflect_index(tx0 - WR + e, a.w);
-                if constexpr (SHADE) s_gx[e] = x;
-                s_xa[e] = clampi(x - op.ix, 0, a.w - 1);
-                s_xb[e] = clampi(x - op.ix - 1, 0, a.w - 1);
-            }
-        }
-        __syncthreads();
-        mbar_wait(&bar, phase);
-        phase ^= 1u;
-        const int bx0 = s_box[0], by0 = s_box[1];
-        // 2. corrected samples on tile + halo (float32, numpy's order); the
-        //    interior goes straight to the corrected output.  Warps walk rows,
-        //    lanes own fixed columns (their x taps cached in registers).
-        {
-            constexpr int NCS = (EW + 31) / 32;
-            const int lane = tid & 31, warp = tid >> 5;
-            int xa[NCS], xb[NCS], gxs[NCS];
-#pragma unroll
-            for (int k = 0; k < NCS; ++k) {
-                const int c = lane + 32 * k;
-                xa[k] = c < EW ? s_xa[c] - bx0 : 0;
-                xb[k] = c < EW ? s_xb[c] - bx0 : 0;
-                if constexpr (SHADE) gxs[k] = c < EW ? s_gx[c] : 0;
-            }
-            auto smp = [](S_T v) -> float {  // u16 -> f32 exactly on the ALU/FMA pipes
-                if constexpr (U16)
-                    return u16_minus(v, 8388608.0f);
-                else
-                    return v;
-            };
-            float* corr_base = a.corrected ? a.corrected + t * hw : nullptr;
-            for (int ey = warp; ey < EH; ey += kK3Threads / 32) {
-                const S_T* ra = sRaw + (s_ra[ey] - by0) * BWB;
-                const S_T* rc = sRaw + (s_rc[ey] - by0) * BWB;
-                const int gy = ty0 + ey - WR;
-                const bool row_out = corr_base && ey >= WR && ey < WR + kTY && gy < a.h;
-                const float* grow = SHADE ? a.gain + (int64_t)s_gy[ey] * a.w : nullptr;
-#pragma unroll
-                for (int k = 0; k < NCS; ++k) {
-                    const int c = lane + 32 * k;
-                    if (c < EW) {
-                        const float top = __fadd_rn(__fmul_rn(op.omx, smp(ra[xa[k]])), __fmul_rn(op.fx, smp(ra[xb[k]])));
-                        const float bot = __fadd_rn(__fmul_rn(op.omx, smp(rc[xa[k]])), __fmul_rn(op.fx, smp(rc[xb[k]])));
-                        float v = __fadd_rn(__fmul_rn(op.omy, top), __fmul_rn(op.fy, bot));
-                        if constexpr (SHADE) v = __fdiv_rn(v, __ldg(grow + gxs[k]));
-                        sC[ey * EWP + c] = (double)v;
-                        const int gx = tx0 + c - WR;
-                        if (row_out && c >= WR && c < WR + kTX && gx < a.w) corr_base[(int64_t)gy * a.w + gx] = v;
-                    }
-                }
-            }
-        }
-        __syncthreads();
-        if (tid == 0 && t + gridDim.z < a.n) origin_next = issue(t + gridDim.z);  // raw box consumed
-        // 3. H (vertical) pass, VR outputs per thread, rounded to f32
-        constexpr int VR = 4, HR = 8;
-        for (int i = tid; i < (kTY / VR) * EW; i += kK3Threads) {
-            const int c = i % EW, r0 = (i / EW) * VR;
-            double x[VR + 2 * WR];
-#pragma unroll
-            for (int q = 0; q < VR + 2 * WR; ++q) x[q] = sC[(r0 + q) * EWP + c];
-#pragma unroll
-            for (int j = 0; j < VR; ++j) {
-                double acc = __dmul_rn(x[j + WR], wk[0]);
-#pragma unroll
-                for (int k = WR; k >= 1; --k) acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(x[j + WR - k], x[j + WR + k]), wk[k]));
-                sV[(r0 + j) * EWP + c] = (double)(float)acc;
-            }
-        }
-        __syncthreads();
-        // 4. W pass -> smoothed frame (time-major).  Lanes take consecutive
-        //    rows (bank-conflict-free float64 reads), each HR consecutive outputs.
-        for (int i = tid; i < kTY * (kTX / HR); i += kK3Threads) {
-            const int ly = i % kTY, lx0 = (i / kTY) * HR;
-            double x[HR + 2 * WR];
-#pragma unroll
-            for (int q = 0; q < HR + 2 * WR; ++q) x[q] = sV[ly * EWP + lx0 + q];
-            const int gy = ty0 + ly;
-            float o[HR];
-#pragma unroll
-            for (int j = 0; j < HR; ++j) {
-                double acc = __dmul_rn(x[j + WR], wk[0]);
-#pragma unroll
-                for (int k = WR; k >= 1; --k) acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(x[j + WR - k], x[j + WR + k]), wk[k]));
-                o[j] = (float)acc;
-            }
-            const int gx0 = tx0 + lx0;
-            float* dst = a.smoothed + t * hw + (int64_t)gy * a.w + gx0;
-            if (gy < a.h) {
-                if ((a.w & 3) == 0 && gx0 + HR <= a.w) {
-#pragma unroll
-                    for (int j = 0; j < HR; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < HR; ++j)
-                        if (gx0 + j < a.w) dst[j] = o[j];
-                }
-            }
-        }
-    }
-}
-
-// K3 v2: same tile, TMA box and float64 operation order as
-// warp_smooth_tma_kernel, restructured for fewer issued instructions (the
-// kernel is issue-bound, not FP64-pipe-bound):
+// K3 v2 (fused warp + smoothing; the fallback of the split form below for
+// widths that are not a multiple of 4 and frames under 10 rows/columns):
+// one CTA per (tile, frame slice), persistent over frames; the elected thread
+// issues the next frame's raw box by TMA (16-byte aligned start, zero-filled
+// out of bounds).  Restructured for few issued instructions:
 //  A1 the bilinear warp is separable -- translate's top/bottom rows are
 //     omx*a + fx*b of source rows ra and rc, and row y+1's bottom row is row
 //     y's top row -- so each raw-box row is interpolated horizontally once
@@ -761,21 +576,9 @@ static_assert(kK3Threads == kTY * (kTX / 8), "horizontal pass maps one thread pe
 static_assert(3 * (kTX + 18) <= kK3Threads, "vertical pass maps one thread per (column, third)");
 
 template <int WR, bool U16>
-static size_t k3_tma_smem_bytes() {
-    constexpr int EH = kTY + 2 * WR, EW = kTX + 2 * WR, EWP = EW | 1;
-    constexpr int ALN = U16 ? 8 : 4;
-    constexpr int BWB = ((EW + 1 + ALN - 1 + ALN - 1) / ALN) * ALN;
-    constexpr int BHB = EH + 1;
-    const size_t raw = (((size_t)BHB * BWB * (U16 ? 2 : 4)) + 127) & ~(size_t)127;
-    return raw + (size_t)(EH + kTY) * EWP * sizeof(double);
-}
-
-template <int WR, bool U16>
 static int launch_k3_tma(const CUtensorMap& tmap, K3Args a, int64_t n, int h, int w, cudaStream_t s) {
-    static const bool v1 = getenv("VB_K3_V1") != nullptr;  // experiment knob: the previous kernel
-    const size_t smem = v1 ? k3_tma_smem_bytes<WR, U16>() : k3_v2_smem_bytes<WR, U16>();
-    auto kern = v1 ? (a.gain ? warp_smooth_tma_kernel<WR, U16, true> : warp_smooth_tma_kernel<WR, U16, false>)
-                   : (a.gain ? warp_smooth_v2_kernel<WR, U16, true> : warp_smooth_v2_kernel<WR, U16, false>);
+    const size_t smem = k3_v2_smem_bytes<WR, U16>();
+    auto kern = a.gain ? warp_smooth_v2_kernel<WR, U16, true> : warp_smooth_v2_kernel<WR, U16, false>;
     VB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -1467,9 +1270,8 @@ static int launch_k3(const void* frames, int dtype, const vb_motion* vec, int64_
     a.wr = wradius;
     a.gain = gain;
     for (int i = 0; i < 2 * wradius + 1; ++i) a.wt.w[i] = weights[i];
-    static const bool no_tma = getenv("VB_NO_TMA") != nullptr;
-    static const char* k3_mode = getenv("VB_K3_SPLIT");  // experiment knob: 0 = fused kernel
-    if (wradius == 9 && !no_tma && !(k3_mode && atoi(k3_mode) == 0)) {
+    const bool no_tma = knob("VB_NO_TMA", 0) != 0;
+    if (wradius == 9 && !no_tma && knob("VB_K3_SPLIT", 1) != 0) {  // experiment: 0 = fused kernel
         const int rc = launch_k3_split(frames, dtype, vec, n, h, w, a, corrected, smoothed, s);
         if (rc != kK3NotHandled) return rc;
     }

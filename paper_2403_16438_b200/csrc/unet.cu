@@ -510,8 +510,7 @@ int launch_conv_tc(const ConvArgs& a, cudaStream_t s) {
 }
 
 int conv(const ConvArgs& a, cudaStream_t s) {
-    static const bool simt = getenv("VB_UNET_SIMT") != nullptr;  // experiment knob: FP32 SIMT kernels
-    if (!simt) {
+    if (!knob("VB_UNET_SIMT", 0)) {  // experiment: FP32 SIMT kernels
         if (a.cout <= 16) return launch_conv_tc<16>(a, s);
         if (a.cout <= 32) return launch_conv_tc<32>(a, s);
         if (a.cout <= 64) return launch_conv_tc<64>(a, s);

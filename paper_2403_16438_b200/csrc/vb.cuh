@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <atomic>
 #include <string>
@@ -17,6 +18,19 @@ int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* where);
 std::atomic<int64_t>& launches();
 void keep_pool();
+
+// A/B experiment switches.  Only an experiment build (build.py --experiments,
+// -DVB_EXPERIMENTS) reads them from the environment; the product library
+// always uses the measured defaults passed here.
+inline int knob(const char* name, int dflt) {
+#ifdef VB_EXPERIMENTS
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+#else
+    (void)name;
+    return dflt;
+#endif
+}
 
 #define VB_CUDA(call)                                               \
     do {                                                            \
@@ -59,6 +73,7 @@ struct PatchGroup {
 
 static constexpr int kMaxRadius = 31;  // _native.pyx:63-66 (acc[63])
 static constexpr int kMaxGroup = 32;
+static constexpr int kMaxPatch = 180;  // integer window-sum range (zncc_stats_kernel)
 
 // Prepared template for one recording (device memory).
 struct Templates {

@@ -288,19 +288,9 @@ def correct_motion(video, config: MotionConfig | None = None) -> tuple[Video, li
 
     sc = S.StageConfig(patch_size=config.patch_size, search_radius=config.search_radius, subpixel=config.subpixel,
                        ref_frames=REFERENCE_FRAMES, shading_sigma=config.shading_sigma)
-    key = (dev.index or 0, v.height, v.width, repr(sc))
-    c = _stage_cache.__dict__
-    if c.get("key") != key:
-        if c.get("hs") is not None:
-            c["hs"].close()
-        c["hs"], c["key"] = None, None
-        c["hs"] = S.HostStage(v.height, v.width, sc, device=dev.index or 0)
-        c["key"] = key
-    rec, _sp, _tp, out = c["hs"].run(v.samples, corrected=True, summaries=False)
+    hs = S.cached_host_stage(dev, v.height, v.width, sc)
+    rec, _sp, _tp, out = hs.run(v.samples, corrected=True, summaries=False)
     return Video._trusted(out, frame_rate=v.frame_rate), _vectors_from_numpy(rec)
-
-
-_stage_cache = threading.local()
 
 
 def correct_frame(frame: np.ndarray, vector: MotionVector) -> np.ndarray:

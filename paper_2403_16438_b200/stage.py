@@ -13,9 +13,10 @@ Three entry points:
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
 import math
-import os
 import threading
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -91,7 +92,7 @@ class DevicePreprocessor:
     # Blocks per pipelined chunk (see search_and_summarize); 0 = serial.
     # Measured on C2: 0 -> 44.3 ms/step, 1..5 -> 44.4-45.8 ms (the SMs are
     # already saturated; concurrent kernels only slow each other), so serial.
-    overlap_blocks = int(os.environ.get("VB_OVERLAP_BLOCKS", "0"))
+    overlap_blocks = 0
 
     def set_shading(self, ref: torch.Tensor) -> None:
         """Flat-field gain of this recording's template (A17; no-op when off)."""
@@ -148,31 +149,27 @@ class DevicePreprocessor:
         self.plan.close()
 
 
-def preprocess(video, config: StageConfig | None = None, return_corrected: bool = True):
+def preprocess(video, config: StageConfig | None = None, return_corrected: bool = True, out=None):
     """correct_motion + summarize in one device pass.
 
     Returns (corrected Video | None, list[MotionVector], list[SummaryPair]) --
     the same values as the reference's correct_motion(video, MotionConfig(...))
-    followed by summarize(corrected, L, sigma)."""
+    followed by summarize(corrected, L, sigma).
+
+    out: optional float32 (T, H, W) C-contiguous host array that receives the
+    corrected video (reused across calls; page-locked arrays -- pinned_empty()
+    -- are filled by direct device->host copies).  Without it the corrected
+    video lands in a page-locked array from the stage's host pool."""
     v = Video.wrap(video)
     dev = D.require_cuda()
     if not (isinstance(v.samples, torch.Tensor) and v.samples.is_cuda):
         # host recording: the C-ABI executor streams it through a two-chunk
         # device ring (bounded HBM, H2D / compute / D2H overlapped, threaded
         # host staging); bit-identical to the device-resident path below
-        # the executor (and its pinned staging ring) is kept per thread for the
-        # last geometry + configuration: repeated calls skip the allocations
-        key = (dev.index or 0, v.height, v.width, repr(config))
-        c = _stage_cache.__dict__
-        if c.get("key") != key:
-            if c.get("hs") is not None:
-                c["hs"].close()
-            c["hs"], c["key"] = None, None
-            c["hs"] = HostStage(v.height, v.width, config, device=dev.index or 0)
-            c["key"] = key
-        rec, sp, tp, corr = c["hs"].run(v.samples, corrected=return_corrected)
-        out = Video._trusted(corr, frame_rate=v.frame_rate) if return_corrected else None
-        return out, M._vectors_from_numpy(rec), [SummaryPair(i, sp[i], tp[i]) for i in range(sp.shape[0])]
+        hs = cached_host_stage(dev, v.height, v.width, config)
+        rec, sp, tp, corr = hs.run(v.samples, corrected=return_corrected, out=out)
+        res = Video._trusted(corr, frame_rate=v.frame_rate) if return_corrected else None
+        return res, M._vectors_from_numpy(rec), [SummaryPair(i, sp[i], tp[i]) for i in range(sp.shape[0])]
     frames = D.as_device_frames(v.samples, dev)
     pre = DevicePreprocessor(v.height, v.width, config)
     try:
@@ -180,15 +177,124 @@ def preprocess(video, config: StageConfig | None = None, return_corrected: bool 
         res = pre.run(frames, corrected_out=corr)
         rec = res.vectors_numpy()
         sp, tp = res.spatial.cpu().numpy(), res.temporal.cpu().numpy()
-        out = Video._trusted(corr.cpu().numpy(), frame_rate=v.frame_rate) if return_corrected else None
+        if return_corrected:
+            host = _check_out(out, tuple(frames.shape)) if out is not None else pinned_empty(tuple(frames.shape))
+            torch.from_numpy(host).copy_(corr)
+        out_v = Video._trusted(host, frame_rate=v.frame_rate) if return_corrected else None
     finally:
         pre.close()
     vectors = M._vectors_from_numpy(rec)
     pairs = [SummaryPair(i, sp[i], tp[i]) for i in range(sp.shape[0])]
-    return out, vectors, pairs
+    return out_v, vectors, pairs
 
 
+# ---- per-thread executor cache (shared by preprocess and motion.correct_motion)
 _stage_cache = threading.local()
+
+
+def _resolved(config: StageConfig | None) -> StageConfig:
+    """The configuration with call-time defaults filled in (ref_frames reads
+    motion.REFERENCE_FRAMES now, as the reference does at each call)."""
+    c = dataclasses.replace(config) if config is not None else StageConfig()
+    if c.ref_frames is None:
+        c.ref_frames = M.REFERENCE_FRAMES
+    return c
+
+
+def cached_host_stage(dev: torch.device, height: int, width: int, config: StageConfig | None) -> "HostStage":
+    """The calling thread's executor for this geometry + resolved configuration
+    (repeated calls skip the device-ring and pinned-slot allocations); a
+    different key replaces it."""
+    c = _resolved(config)
+    key = (dev.index or 0, height, width, repr(c))
+    cache = _stage_cache.__dict__
+    if cache.get("key") != key:
+        if cache.get("hs") is not None:
+            cache["hs"].close()
+        cache["hs"], cache["key"] = None, None
+        cache["hs"] = HostStage(height, width, c, device=dev.index or 0)
+        cache["key"] = key
+    return cache["hs"]
+
+
+def release_cached() -> None:
+    """Free the calling thread's cached executor (device ring, pinned staging)
+    and the idle page-locked output buffers of the host pool."""
+    cache = _stage_cache.__dict__
+    if cache.get("hs") is not None:
+        cache["hs"].close()
+    cache["hs"], cache["key"] = None, None
+    _POOL.trim(0)
+
+
+# ---- page-locked output buffers -------------------------------------------
+class _PinnedBlock:
+    """One vb_host_alloc block exposed through the array interface; the
+    numpy arrays made from it keep it alive, and when the last one goes the
+    block returns to its pool."""
+
+    def __init__(self, pool: "PinnedPool", ptr: int, nbytes: int, shape: tuple, dtype: np.dtype):
+        self.__array_interface__ = {"data": (ptr, False), "shape": shape, "typestr": dtype.str, "version": 3}
+        weakref.finalize(self, pool._release, ptr, nbytes)
+
+
+class PinnedPool:
+    """Reuses page-locked host blocks of equal size: allocating and first-touching
+    gigabytes of output per call costs more than the PCIe transfer into them,
+    and page-locked memory is what lets the executor copy device->host straight
+    into the caller's array.  At most `keep` idle blocks are retained."""
+
+    def __init__(self, keep: int = 2):
+        self.keep = keep
+        self._idle: list[tuple[int, int]] = []  # (nbytes, ptr), most recent last
+        self._lock = threading.Lock()
+
+    def empty(self, shape: tuple, dtype=np.float32) -> np.ndarray:
+        dtype = np.dtype(dtype)
+        nbytes = int(np.prod(shape)) * dtype.itemsize
+        if nbytes == 0:
+            return np.empty(shape, dtype)
+        ptr = None
+        with self._lock:
+            for i in range(len(self._idle) - 1, -1, -1):
+                if self._idle[i][0] == nbytes:
+                    ptr = self._idle.pop(i)[1]
+                    break
+        if ptr is None:
+            p = C.c_void_p()
+            rc = _lib.load().vb_host_alloc(nbytes, C.byref(p))
+            if rc != _lib.VB_OK:
+                self.trim(0)  # retry once with the idle blocks released
+                _lib.call("vb_host_alloc", nbytes, C.byref(p))
+            ptr = p.value
+        return np.asarray(_PinnedBlock(self, ptr, nbytes, tuple(shape), dtype))
+
+    def _release(self, ptr: int, nbytes: int) -> None:
+        with self._lock:
+            self._idle.append((nbytes, ptr))
+        self.trim(self.keep)
+
+    def trim(self, keep: int) -> None:
+        with self._lock:
+            drop = self._idle[:max(0, len(self._idle) - keep)]
+            self._idle = self._idle[len(drop):]
+        for _, ptr in drop:
+            _lib.load().vb_host_free(ptr)
+
+
+_POOL = PinnedPool()
+
+
+def pinned_empty(shape: tuple, dtype=np.float32) -> np.ndarray:
+    """A page-locked host array from the stage's pool (see PinnedPool)."""
+    return _POOL.empty(shape, dtype)
+
+
+def _check_out(out, shape: tuple) -> np.ndarray:
+    if not isinstance(out, np.ndarray) or out.dtype != np.float32 or out.shape != shape \
+            or not out.flags.c_contiguous or not out.flags.writeable:
+        raise ValueError(f"out must be a writeable C-contiguous float32 array of shape {shape}")
+    return out
 
 
 class HostStage:
@@ -214,10 +320,12 @@ class HostStage:
             _lib.call("vb_stage_set_shading", self._h, self._sw.ctypes.data, sr)
         self.height, self.width = height, width
 
-    def run(self, frames: np.ndarray, corrected: bool = False, summaries: bool = True):
+    def run(self, frames: np.ndarray, corrected: bool = False, summaries: bool = True, out=None):
         """frames: uint16/float32 (T,H,W) host array (pinned or pageable).
         Returns (vectors record array, spatial [K,H,W], temporal [K,H,W], corrected|None);
-        summaries=False: motion only (spatial / temporal are None)."""
+        summaries=False: motion only (spatial / temporal are None).  The
+        corrected video goes into `out` when given, else into a page-locked
+        array from the host pool (direct device->host copies)."""
         a = frames
         if isinstance(a, torch.Tensor):
             assert not a.is_cuda
@@ -233,7 +341,10 @@ class HostStage:
         vec = np.empty(t, dtype=_lib.MOTION_DTYPE)
         sp = np.empty((k, self.height, self.width), np.float32) if summaries else None
         tp = np.empty((k, self.height, self.width), np.float32) if summaries else None
-        corr = np.empty((t, self.height, self.width), np.float32) if corrected else None
+        corr = None
+        if corrected:
+            shape = (t, self.height, self.width)
+            corr = _check_out(out, shape) if out is not None else pinned_empty(shape)
         self.run_into(ptr, dtype, t, vec, sp, tp, corr)
         return vec, sp, tp, corr
 

@@ -53,3 +53,19 @@ def test_version_and_error_without_gpu():
     rc = lib.vb_patch_grid(30, 30, 21, 10, None, ctypes.byref(n))  # host-only geometry, reference message
     assert rc == _lib.VB_EINVAL and b"too small for patch 21 with margin 10" in lib.vb_last_error()
     assert lib.vb_patch_grid(256, 512, 21, 8, None, ctypes.byref(n)) == 0 and n.value == 288
+
+
+def test_host_copy_every_split():
+    """The executor's threaded pageable staging copy (stage.cu host_copy_n)
+    moves every byte for odd frame sizes and 1-8 threads (a split
+    with step = round64(bytes / nt) dropped the last bytes % nt bytes)."""
+    import numpy as np
+
+    lib = _lib.load()
+    rng = np.random.default_rng(5)
+    for n in (299 * 255 * 2 * 250, 341 * 257 * 2 * 250, 213 * 513 * 2 * 250, 100, 64 * 1000003 + 7):
+        a = rng.integers(0, 256, n, dtype=np.uint8)
+        for nt in range(1, 9):
+            b = np.zeros(n, np.uint8)
+            assert lib.vb_host_copy(b.ctypes.data, a.ctypes.data, n, nt) == 0
+            assert np.array_equal(a, b), (n, nt)

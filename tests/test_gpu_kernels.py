@@ -23,7 +23,8 @@ def test_random_frames_vs_oracle(cuda, oracle_mod, rng, radius):
 
 
 @pytest.mark.parametrize("patch,radius,shape", [(15, 3, (60, 60)), (16, 3, (96, 96)), (11, 2, (40, 44)),
-                                                 (5, 1, (20, 23)), (33, 4, (100, 90)), (21, 0, (50, 50))])
+                                                 (5, 1, (20, 23)), (33, 4, (100, 90)), (21, 0, (50, 50)),
+                                                 (65, 3, (150, 150)), (80, 2, (170, 168))])
 def test_generic_patch_sizes(cuda, oracle_mod, rng, patch, radius, shape):
     f = rng.random(shape, dtype=np.float32)
     r = rng.random(shape, dtype=np.float32)
@@ -81,3 +82,35 @@ def test_golden_scores(cuda, golden):
         np.testing.assert_allclose(got, z[f"{name}__py"], atol=1e-6, err_msg=name)
         # integer argmax agrees with both reference backends
         assert np.unravel_index(np.argmax(got), got.shape) == np.unravel_index(np.argmax(z[f"{name}__py"]), got.shape)
+
+
+@pytest.mark.parametrize("patch,radius", [(65, 3), (80, 2)])
+def test_large_patch_full_range_u16(cuda, oracle_mod, rng, patch, radius):
+    """Patches beyond 64 (the window sums loop to P) on full-range uint16
+    samples, where n*var exceeds 2^52 and the int64 -> double conversion
+    must not use the bit trick."""
+    from paper_2403_16438_b200 import _device as D
+    from paper_2403_16438_b200.motion import MotionPlan
+
+    size = patch + 2 * radius + 40
+    fu = rng.integers(0, 65536, (2, size, size), dtype=np.uint16)  # integer window-sum path (u16)
+    r = rng.integers(0, 65536, (size, size)).astype(np.float32)
+    g = PatchGrid.cover(size, size, patch, margin=radius)
+    plan = MotionPlan(size, size, g.origins, patch, radius)
+    try:
+        plan.set_reference(D.as_device_frames(r))
+        _, sc = plan.estimate(D.as_device_frames(fu), True, scores=True)
+        got = sc.cpu().numpy().reshape(2, 2 * radius + 1, 2 * radius + 1)
+    finally:
+        plan.close()
+    for t in range(2):
+        want = oracle_mod.mean_zncc_scores(fu[t].astype(np.float32), r, g.origins, patch, radius)
+        np.testing.assert_allclose(got[t], want, atol=1e-6)
+        np.testing.assert_allclose(kernels.mean_zncc_scores(fu[t].astype(np.float32), r, g.origins, patch, radius),
+                                   want, atol=1e-6)
+
+
+def test_patch_too_large_rejected(cuda, rng):
+    f = rng.random((400, 400), dtype=np.float32)
+    with pytest.raises(ValueError, match="max 180"):
+        kernels.mean_zncc_scores(f, f, np.array([[100, 100]], np.int32), 181, 1)

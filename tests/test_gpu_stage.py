@@ -282,3 +282,55 @@ def test_partial_tiles_warp_and_smooth_vs_oracle(cuda, oracle_mod, c1_small, sha
         blk = corrected.data[40 * i:40 * (i + 1)]
         np.testing.assert_array_equal(p.spatial, oracle_mod.spatial_summary(blk))
         np.testing.assert_array_equal(p.temporal, oracle_mod.temporal_summary(blk))
+
+
+def test_cached_executor_reads_reference_frames_per_call(cuda, c1_small, monkeypatch):
+    """preprocess / correct_motion keep one executor per thread; a config with
+    ref_frames=None must still read motion.REFERENCE_FRAMES at each call
+    (motion.py:24 semantics) -- the cache key holds the resolved value."""
+    from paper_2403_16438_b200 import stage
+
+    cfg, raw = c1_small
+    sc = StageConfig(search_radius=cfg.radius, segment_length=100)  # ref_frames=None
+    monkeypatch.setattr(motion, "REFERENCE_FRAMES", 10)
+    _, v10, _ = preprocess(Video(raw), sc)
+    monkeypatch.setattr(motion, "REFERENCE_FRAMES", 100)
+    _, v100, p100 = preprocess(Video(raw), sc)
+    dev = DevicePreprocessor(raw.shape[1], raw.shape[2], StageConfig(search_radius=cfg.radius, segment_length=100,
+                                                                     ref_frames=100))
+    res = dev.run(D.as_device_frames(raw))
+    want = motion._vectors_from_numpy(res.vectors_numpy())
+    dev.close()
+    assert v100 == want and v10 != v100
+    # the motion-only API shares the cached executor and follows the same rule
+    c2, v2 = motion.correct_motion(Video(raw), motion.MotionConfig(search_radius=cfg.radius))
+    assert v2 == v100
+    stage.release_cached()
+
+
+def test_corrected_output_pinned_pool_and_out(cuda, c1_small):
+    """The corrected video lands in page-locked arrays from the host pool
+    (direct device->host copies) or in a caller's `out=` array; identical
+    values either way, and pool blocks are reused once released."""
+    from paper_2403_16438_b200 import stage
+
+    cfg, raw = c1_small
+    sc = _stage_cfg(cfg, 100)
+    a, va, pa = preprocess(Video(raw), sc)
+    ptr_a = a.data.ctypes.data
+    ref = a.data.copy()
+    del a
+    b, vb, _ = preprocess(Video(raw), sc)
+    assert b.data.ctypes.data == ptr_a  # the released block came back
+    np.testing.assert_array_equal(b.data, ref)
+    out = np.full(raw.shape, -1.0, np.float32)  # pageable caller buffer
+    c, vc, _ = preprocess(Video(raw), sc, out=out)
+    assert c.data is out or c.data.base is out or np.shares_memory(c.data, out)
+    np.testing.assert_array_equal(out, ref)
+    pinned = stage.pinned_empty(raw.shape)
+    preprocess(Video(raw), sc, out=pinned)
+    np.testing.assert_array_equal(pinned, ref)
+    assert va == vb == vc
+    with pytest.raises(ValueError, match="out must be"):
+        preprocess(Video(raw), sc, out=np.empty((1, 2, 3), np.float32))
+    stage.release_cached()
