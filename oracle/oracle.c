@@ -17,6 +17,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+typedef double v4d __attribute__((vector_size(32)));  /* lane-wise IEEE double ops */
+
 static inline int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 /* motion.py:211-214: video.data[:n].mean(axis=0, dtype=float64).astype(float32).
@@ -86,8 +88,31 @@ int or_mean_zncc_scores(const float* frame, const float* ref, int h, int w,
             }
         double rvar = rsq - rsum * rsum / nn;
         if (!(rvar > 0.0)) continue;    /* kernels.py:52 live mask; z stays 0 */
-        for (int dy = -radius; dy <= radius; dy++)
-            for (int dx = -radius; dx <= radius; dx++) {
+        for (int dy = -radius; dy <= radius; dy++) {
+            int dx = -radius;
+            /* four candidates dx..dx+3 at a time: each lane accumulates its own
+             * candidate's sums in the same (yy, xx) order as the scalar loop
+             * below, so the results are bit-identical to it (speed only) */
+            for (; dx + 3 <= radius; dx += 4) {
+                v4d cross = {0, 0, 0, 0}, fs = {0, 0, 0, 0}, fq = {0, 0, 0, 0};
+                for (int yy = 0; yy < patch; yy++) {
+                    const float* fr = frame + (size_t)(py + dy + yy) * w + px + dx;
+                    const float* rr = ref + (size_t)(py + yy) * w + px;
+                    for (int xx = 0; xx < patch; xx++) {
+                        v4d f = {(double)fr[xx], (double)fr[xx + 1], (double)fr[xx + 2], (double)fr[xx + 3]};
+                        double r = (double)rr[xx];
+                        v4d rv = {r, r, r, r};
+                        cross += rv * f; fs += f; fq += f * f;
+                    }
+                }
+                for (int l = 0; l < 4; l++) {
+                    double fvar = fq[l] - fs[l] * fs[l] / nn;
+                    if (!(fvar > 0.0)) continue;
+                    double cov = cross[l] - fs[l] * rsum / nn;
+                    out[(size_t)(dy + radius) * side + dx + l + radius] += cov / sqrt(fvar * rvar);
+                }
+            }
+            for (; dx <= radius; dx++) {
                 double cross = 0.0, fs = 0.0, fq = 0.0;
                 for (int yy = 0; yy < patch; yy++) {
                     const float* fr = frame + (size_t)(py + dy + yy) * w + px + dx;
@@ -102,6 +127,7 @@ int or_mean_zncc_scores(const float* frame, const float* ref, int h, int w,
                 double cov = cross - fs * rsum / nn;      /* kernels.py:68 */
                 out[(size_t)(dy + radius) * side + dx + radius] += cov / sqrt(fvar * rvar);
             }
+        }
     }
     for (int k = 0; k < side * side; k++) out[k] /= (double)n;   /* kernels.py:73 z.sum()/N */
     return 0;
@@ -338,19 +364,49 @@ int or_highpass_summary(const float* corrected, int T, int h, int w, const doubl
 
 /* ---- whole stage ------------------------------------------------------- */
 
+/* ---- threaded drivers (same per-frame / per-pixel arithmetic) ------------ */
+
+typedef struct {
+    void (*fn)(void* ctx, long lo, long hi);
+    void* ctx;
+    long lo, hi;
+} range_job;
+
+static void* range_worker(void* arg) {
+    range_job* j = (range_job*)arg;
+    j->fn(j->ctx, j->lo, j->hi);
+    return NULL;
+}
+
+/* fn(ctx, lo, hi) over [0, n) split into nthreads contiguous ranges. */
+static void parallel_for(long n, int nthreads, void (*fn)(void*, long, long), void* ctx) {
+    if (nthreads > n) nthreads = (int)n;
+    if (nthreads <= 1) { if (n > 0) fn(ctx, 0, n); return; }
+    pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)nthreads);
+    range_job* jobs = (range_job*)malloc(sizeof(range_job) * (size_t)nthreads);
+    for (int k = 0; k < nthreads; k++) {
+        range_job j = {fn, ctx, n * k / nthreads, n * (k + 1) / nthreads};
+        jobs[k] = j;
+        pthread_create(&th[k], NULL, range_worker, &jobs[k]);
+    }
+    for (int k = 0; k < nthreads; k++) pthread_join(th[k], NULL);
+    free(th); free(jobs);
+}
+
 typedef struct {
     const float* frames; const float* ref; const int32_t* origins;
-    int h, w, n, patch, radius, subpixel, t0, t1;
-    int32_t* dxdy; double* sub_conf; float* corrected;
-} motion_job;
+    int h, w, n, patch, radius, subpixel;
+    int32_t* dxdy; double* sub_conf; float* corrected; double* scores;
+} motion_ctx;
 
-static void* motion_worker(void* arg) {
-    motion_job* j = (motion_job*)arg;
+static void motion_range(void* arg, long t0, long t1) {
+    motion_ctx* j = (motion_ctx*)arg;
     int side = 2 * j->radius + 1;
-    double* scores = (double*)malloc(sizeof(double) * (size_t)side * side);
+    double* own = (double*)malloc(sizeof(double) * (size_t)side * side);
     size_t px = (size_t)j->h * j->w;
-    for (int t = j->t0; t < j->t1; t++) {
+    for (long t = t0; t < t1; t++) {
         const float* f = j->frames + (size_t)t * px;
+        double* scores = j->scores ? j->scores + (size_t)t * side * side : own;
         or_mean_zncc_scores(f, j->ref, j->h, j->w, j->origins, j->n, j->patch, j->radius, scores);
         or_pick_motion(scores, j->radius, j->subpixel, j->dxdy + 2 * t, j->sub_conf + 3 * t);
         if (j->corrected) {
@@ -359,8 +415,78 @@ static void* motion_worker(void* arg) {
             or_correct_frame(f, j->h, j->w, vx, vy, j->corrected + (size_t)t * px);
         }
     }
-    free(scores);
-    return NULL;
+    free(own);
+}
+
+int or_motion_frames(const float* frames, int t, int h, int w, const float* ref,
+                     const int32_t* origins, int n, int patch, int radius, int subpixel, int nthreads,
+                     int32_t* dxdy, double* sub_conf, float* corrected, double* scores) {
+    if (radius < 1) return -1;
+    for (int i = 0; i < n; i++) {
+        int x = origins[2 * i], y = origins[2 * i + 1];
+        if (x - radius < 0 || y - radius < 0 || x + patch + radius > w || y + patch + radius > h) return -1;
+    }
+    motion_ctx c = {frames, ref, origins, h, w, n, patch, radius, subpixel, dxdy, sub_conf, corrected, scores};
+    parallel_for(t, nthreads, motion_range, &c);
+    return 0;
+}
+
+typedef struct {
+    const float* in; float* out; int h, w, n; const double* weights; int radius;
+    float* spatial; float* temporal;
+} summ_ctx;
+
+static void smooth_range(void* arg, long t0, long t1) {
+    summ_ctx* c = (summ_ctx*)arg;
+    size_t px = (size_t)c->h * c->w;
+    double* scratch = (double*)malloc(sizeof(double) * px);
+    for (long t = t0; t < t1; t++)
+        or_smooth_frame(c->in + (size_t)t * px, c->h, c->w, c->weights, c->radius, c->out + (size_t)t * px, scratch);
+    free(scratch);
+}
+
+/* summarize.py:55-57 and :76-92 per pixel (the smoothed stack in c->out). */
+static void pixel_range(void* arg, long i0, long i1) {
+    summ_ctx* c = (summ_ctx*)arg;
+    size_t px = (size_t)c->h * c->w;
+    int n = c->n, mid = n / 2;
+    float* col = (float*)malloc(sizeof(float) * (size_t)n);
+    for (long i = i0; i < i1; i++) {
+        double acc = 0.0;
+        for (int t = 0; t < n; t++) acc += (double)c->in[(size_t)t * px + i];
+        c->spatial[i] = (float)(acc / (double)n);
+        if (n < 2) continue;
+        const float* sm = c->out;
+        float peak = sm[i];
+        for (int t = 0; t < n; t++) { col[t] = sm[(size_t)t * px + i]; if (col[t] > peak) peak = col[t]; }
+        qsort(col, (size_t)n, sizeof(float), cmp_float);
+        float med = (n % 2) ? col[mid] : (col[mid - 1] + col[mid]) * 0.5f;
+        c->temporal[i] = peak - med;
+    }
+    free(col);
+}
+
+/* summarize.py:95-102 over corrected frames [t][h][w]: one (spatial, temporal)
+ * pair per block of segment_length frames; a 1-frame tail returns -1 (the
+ * reference raises).  Frames are smoothed in parallel, pixels reduced in
+ * parallel; the arithmetic per frame / pixel is or_smooth_frame /
+ * or_spatial_summary / or_temporal_summary's. */
+int or_summaries(const float* corrected, int t, int h, int w, int segment_length,
+                 const double* weights, int wradius, int nthreads, float* spatial, float* temporal) {
+    if (segment_length < 2) return -1;
+    size_t px = (size_t)h * w;
+    int nseg = (t + segment_length - 1) / segment_length;
+    if (t - (nseg - 1) * segment_length < 2) return -1;
+    float* sm = (float*)malloc(sizeof(float) * px * (size_t)(t < segment_length ? t : segment_length));
+    for (int s = 0; s < nseg; s++) {
+        int lo = s * segment_length, hi = lo + segment_length < t ? lo + segment_length : t;
+        summ_ctx c = {corrected + (size_t)lo * px, sm, h, w, hi - lo, weights, wradius,
+                      spatial + (size_t)s * px, temporal + (size_t)s * px};
+        parallel_for(hi - lo, nthreads, smooth_range, &c);
+        parallel_for((long)px, nthreads, pixel_range, &c);
+    }
+    free(sm);
+    return 0;
 }
 
 int or_preprocess(const float* frames, int t, int h, int w, int patch, int radius,
@@ -379,18 +505,7 @@ int or_preprocess(const float* frames, int t, int h, int w, int patch, int radiu
     int own = corrected == NULL;
     float* corr = own ? (float*)malloc(sizeof(float) * px * (size_t)t) : corrected;
     if (nthreads < 1) nthreads = 1;
-    if (nthreads > t) nthreads = t;
-    pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)nthreads);
-    motion_job* jobs = (motion_job*)malloc(sizeof(motion_job) * (size_t)nthreads);
-    for (int k = 0; k < nthreads; k++) {
-        motion_job j = {frames, ref, origins, h, w, n, patch, radius, subpixel,
-                        (int)((long)t * k / nthreads), (int)((long)t * (k + 1) / nthreads),
-                        dxdy, sub_conf, corr};
-        jobs[k] = j;
-        pthread_create(&th[k], NULL, motion_worker, &jobs[k]);
-    }
-    for (int k = 0; k < nthreads; k++) pthread_join(th[k], NULL);
-    free(th); free(jobs);
+    or_motion_frames(frames, t, h, w, ref, origins, n, patch, radius, subpixel, nthreads, dxdy, sub_conf, corr, NULL);
     int nseg = (t + segment_length - 1) / segment_length;
     for (int s = 0; s < nseg; s++) {
         int lo = s * segment_length, hi = lo + segment_length < t ? lo + segment_length : t;

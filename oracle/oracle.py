@@ -58,6 +58,11 @@ def lib():
         L.or_highpass_summary.argtypes = [_f32p, C.c_int, C.c_int, C.c_int, _f64p, C.c_int, C.c_int, C.c_int,
                                           _f32p]
         L.or_highpass_summary.restype = C.c_int
+        L.or_motion_frames.argtypes = [_f32p, C.c_int, C.c_int, C.c_int, _f32p, _i32p, C.c_int, C.c_int, C.c_int,
+                                       C.c_int, C.c_int, _i32p, _f64p, C.c_void_p, C.c_void_p]
+        L.or_motion_frames.restype = C.c_int
+        L.or_summaries.argtypes = [_f32p, C.c_int, C.c_int, C.c_int, C.c_int, _f64p, C.c_int, C.c_int, _f32p, _f32p]
+        L.or_summaries.restype = C.c_int
         _lib = L
     return _lib
 
@@ -190,6 +195,43 @@ def preprocess(frames, patch=21, radius=10, subpixel=True, ref_frames=50,
     if rc != 0:
         raise ValueError("invalid preprocess geometry")
     return dict(dxdy=dxdy, sub_conf=sc, corrected=corr, spatial=sp, temporal=tp)
+
+
+def motion_frames(frames, reference, origins, patch: int, radius: int, subpixel: bool = True,
+                  threads: int | None = None, want_corrected: bool = True, want_scores: bool = False):
+    """estimate_motion + correct_frame (motion.py:113-160, :235-240) of every
+    frame against a given template, frames split over threads.
+
+    Returns dict(dxdy int32[T,2], sub_conf f64[T,3], corrected f32[T,H,W] | None,
+    scores f64[T,2r+1,2r+1] | None)."""
+    f = _f32(frames)
+    t, h, w = f.shape
+    o = np.ascontiguousarray(origins, dtype=np.int32)
+    dxdy = np.empty((t, 2), np.int32)
+    sc = np.empty((t, 3), np.float64)
+    corr = np.empty_like(f) if want_corrected else None
+    side = 2 * radius + 1
+    scores = np.empty((t, side, side), np.float64) if want_scores else None
+    rc = lib().or_motion_frames(f, t, h, w, _f32(reference), o, len(o), patch, radius, int(subpixel),
+                                threads or os.cpu_count() or 1, dxdy, sc,
+                                corr.ctypes.data if corr is not None else None,
+                                scores.ctypes.data if scores is not None else None)
+    if rc != 0:
+        raise ValueError("patch origin too close to border for search radius")
+    return dict(dxdy=dxdy, sub_conf=sc, corrected=corr, scores=scores)
+
+
+def summaries(corrected, segment_length: int, sigma: float = 3.0, threads: int | None = None):
+    """summarize.py:95-102 over corrected frames -> (spatial f32[K,H,W], temporal f32[K,H,W])."""
+    f = _f32(corrected)
+    t, h, w = f.shape
+    k = -(-t // segment_length)
+    wts, wr = gaussian_weights(sigma)
+    sp = np.empty((k, h, w), np.float32)
+    tp = np.empty((k, h, w), np.float32)
+    if lib().or_summaries(f, t, h, w, segment_length, wts, wr, threads or os.cpu_count() or 1, sp, tp) != 0:
+        raise ValueError("temporal summary needs at least 2 frames")
+    return sp, tp
 
 
 def extract_trace(frames, mask) -> np.ndarray:
