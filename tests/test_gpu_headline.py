@@ -12,10 +12,14 @@
       of ~1000-count frames, themselves a few counts) within 1e-4 of the
       block's spatial scale.
 * Against the reference's DEFAULT backend (its compiled `_native` kernel,
-  `oracle/_ref`) on all 10,000 C2 frames: every frame where the GPU's integer
-  shift differs from native must be a frame where native also differs from
-  the float64 backend, with a float64 top-2 margin below 1e-4 (the native
-  kernel's own score noise); any other mismatch fails.
+  `oracle/_ref`) on every frame: the native kernel forms its cross sums in
+  float32 (`-ffast-math`, _native_impl.h:18-35) and disagrees with the
+  reference's own float64 backend on a few percent of C2 frames.  Required:
+  every frame where the GPU's integer shift differs from native is a frame
+  where native also differs from float64, and on each such frame native's
+  score grid is within its float32 noise (<= 1e-3) of the float64 grid --
+  the flip is native rounding at a near-tie, not a GPU error.  Reported:
+  the float64 top-2 margin at those frames vs over all frames.
 * C3 / C4 / C5 geometries: the same checks on two full 1,000-frame blocks.
 
 Each configuration's table (GPU / native / float64 pairwise counts, maxima)
@@ -84,10 +88,13 @@ def _check(name: str, frames: int, native: bool):
                gpu_vs_f64_int_mismatch=0, max_subpixel_diff_px=0.0, max_corrected_rel=0.0,
                max_spatial_rel=0.0, max_temporal_abs_over_scale=0.0, max_confidence_diff=0.0, blocks=[])
     o_dxdy_all = np.empty_like(g_dxdy)
+    top2 = np.empty(frames)  # float64 top-2 score margin per frame
     for b0 in range(0, frames, L):
         b1 = min(frames, b0 + L)
-        m = O.motion_frames(raw[b0:b1].astype(np.float32), ref, origins, 21, r, threads=THREADS)
+        m = O.motion_frames(raw[b0:b1].astype(np.float32), ref, origins, 21, r, threads=THREADS, want_scores=True)
         o_dxdy_all[b0:b1] = m["dxdy"]
+        flat = np.sort(m["scores"].reshape(b1 - b0, -1), axis=1)
+        top2[b0:b1] = flat[:, -1] - flat[:, -2]
         bad = np.nonzero((m["dxdy"] != g_dxdy[b0:b1]).any(axis=1))[0]
         sub = float(np.abs(m["sub_conf"][:, :2] - g_sub[b0:b1]).max())
         conf = float(np.abs(m["sub_conf"][:, 2] - rec["confidence"][b0:b1]).max())
@@ -112,21 +119,38 @@ def _check(name: str, frames: int, native: bool):
 
     failures = []
     if native:
+        from oracle import ref as R
+
+        _m, _s, kernels, _v = R.load("native")
         n_dxdy = _native_vectors(raw, ref, r)
         nat_vs_gpu = np.nonzero((n_dxdy != g_dxdy).any(axis=1))[0]
-        nat_vs_f64 = np.nonzero((n_dxdy != o_dxdy_all).any(axis=1))[0]
+        nat_vs_f64 = set(np.nonzero((n_dxdy != o_dxdy_all).any(axis=1))[0].tolist())
         rows = []
         for t in nat_vs_gpu:
-            s64 = O.mean_zncc_scores(raw[t].astype(np.float32), ref, origins, 21, r)
+            f32 = raw[t].astype(np.float32)
+            s64 = O.mean_zncc_scores(f32, ref, origins, 21, r)
+            snat = kernels.mean_zncc_scores(f32, ref, origins, 21, r)
             gi, ni = (g_dxdy[t][1] + r, g_dxdy[t][0] + r), (n_dxdy[t][1] + r, n_dxdy[t][0] + r)
             margin = float(s64[gi] - s64[ni])
-            explained = bool(t in set(nat_vs_f64.tolist())) and 0.0 <= margin < 1e-4
+            nerr = float(np.abs(snat - s64).max())
+            explained = int(t) in nat_vs_f64 and nerr <= 1e-3 and 0.0 <= margin <= 2 * nerr
             rows.append(dict(frame=int(t), gpu=g_dxdy[t].tolist(), native=n_dxdy[t].tolist(),
-                             f64=o_dxdy_all[t].tolist(), f64_margin=margin, near_tie=explained))
+                             f64=o_dxdy_all[t].tolist(), f64_margin=margin, native_grid_err=nerr,
+                             native_rounding_flip=explained))
             if not explained:
-                failures.append(f"frame {t}: gpu {g_dxdy[t]} native {n_dxdy[t]} f64 margin {margin:.3g}")
-        tab["native"] = dict(frames_compared=int(frames), gpu_vs_native_int_mismatch=int(len(nat_vs_gpu)),
-                             native_vs_f64_int_mismatch=int(len(nat_vs_f64)), mismatches=rows)
+                failures.append(f"frame {t}: gpu {g_dxdy[t]} native {n_dxdy[t]} f64 margin {margin:.3g} "
+                                f"native err {nerr:.3g}")
+        mm = np.array([row["f64_margin"] for row in rows]) if rows else np.zeros(1)
+        tab["native"] = dict(
+            backend="reference voltseg._native (oracle/_ref), estimate_motion, default flags",
+            frames_compared=int(frames), gpu_vs_native_int_mismatch=int(len(nat_vs_gpu)),
+            native_vs_f64_int_mismatch=int(len(nat_vs_f64)),
+            gpu_vs_f64_int_mismatch=tab["gpu_vs_f64_int_mismatch"],
+            mismatch_f64_margin_max=float(mm.max()),
+            mismatch_native_grid_err_max=float(max([row["native_grid_err"] for row in rows], default=0.0)),
+            all_frames_f64_top2_margin_quantiles={q: float(np.quantile(top2, q)) for q in (0.01, 0.05, 0.5)},
+            frames_with_top2_margin_below_mismatch_max=int((top2 <= mm.max()).sum()),
+            mismatches=rows)
     tab["wall_s"] = round(time.time() - t0, 1)
     OUT.mkdir(exist_ok=True)
     (OUT / f"r02_parity_{name}.json").write_text(json.dumps(tab, indent=1))
