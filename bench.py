@@ -12,9 +12,18 @@ spatial mean / smoothing / max-minus-median, corrected video written to HBM.
 `value` = frames processed by all ranks / max-over-ranks device time (inputs
 resident in HBM, CUDA events).  `e2e` = the same through the C-ABI host entry
 point vb_stage_run_host with pinned host input (H2D of every frame, D2H of
-vectors + summaries inside the timed region).  Under torchrun each rank
-takes its own shard (weak scaling).  `--impl reference` times the unmodified
-reference (voltseg, oracle/_ref) on the host CPU cores on the same workload.
+vectors + summaries inside the timed region).  `e2e_dropin` = the drop-in
+Python API (stage.preprocess) from a plain numpy uint16 recording to the
+corrected float32 video, vectors and summaries on the host -- what the
+reference's correct_motion + summarize return.
+
+--gpus N > 1 without a torchrun environment re-launches itself under
+torchrun (one process per GPU).  N > 1 defaults to strong scaling: the one
+10,000-frame recording split into frame-balanced time shards, blocks that
+straddle two ranks exchanged over peer memory; --scaling weak gives every rank
+its own 10,000-frame shard.  `--impl reference` times the unmodified
+reference (voltseg, oracle/_ref) on the host CPU cores, one full L-frame block
+of the same recording per step (blocks in turn).
 """
 from __future__ import annotations
 
@@ -54,11 +63,33 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-corrected", action="store_true", help="do not materialise the corrected video")
     p.add_argument("--cpu-sample", type=int, default=2000, help="frames in the CPU baseline sample (~10 s of CPU work on C2)")
-    p.add_argument("--ref-step-frames", type=int, default=400, help="frames per --impl reference step")
-    p.add_argument("--scaling", choices=["weak", "strong"], default="weak",
-                   help="weak: each rank owns its own T-frame recording shard; strong: one T-frame recording "
-                        "split into frame-balanced shards (blocks straddling ranks are exchanged over NCCL)")
+    p.add_argument("--ref-step-frames", type=int, default=0,
+                   help="frames per --impl reference step (default: one full block, L frames)")
+    p.add_argument("--scaling", choices=["weak", "strong"], default=None,
+                   help="weak: each rank owns its own T-frame recording shard; strong (default for N > 1): one "
+                        "T-frame recording split into frame-balanced shards (straddling blocks exchanged over "
+                        "peer memory)")
+    p.add_argument("--no-dropin", action="store_true", help="skip the drop-in Python API e2e leg")
     return p.parse_args()
+
+
+def free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch_under_torchrun(args) -> int | None:
+    """--gpus N > 1 outside torchrun: re-run this command as N ranks (one process
+    per GPU, rendezvous on 127.0.0.1); rank 0 prints the JSON line."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def dist_env():
@@ -201,18 +232,27 @@ def run_reference(args):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    n = min(args.ref_step_frames, cfg.frames)
-    frames = host_sample(cfg, n)
+    n = min(args.ref_step_frames or cfg.segment_length, cfg.frames)
+    # the whole recording on the host; step i runs the reference stage on block
+    # (W + i) mod K -- one full L-frame block per step, so K steps cover it all
+    rec = host_sample(cfg, cfg.frames)
+    nblk = max(1, cfg.frames // n)
     kind = "reference"
     try:
         from oracle import ref as _r
 
         if not _r.available():
             raise RuntimeError("oracle/_ref missing")
-        step = lambda: reference_stage_fps(frames, cfg, threads)[1]  # noqa: E731
+        fn = lambda x: reference_stage_fps(x, cfg, threads)[1]  # noqa: E731
     except Exception:  # reference not built: oracle port (C restatement)
         kind = "port"
-        step = lambda: oracle_port_fps(frames, cfg, threads)[1]  # noqa: E731
+        fn = lambda x: oracle_port_fps(x, cfg, threads)[1]  # noqa: E731
+    it = iter(range(10 ** 9))
+
+    def step():
+        b = next(it) % nblk
+        return fn(rec[b * n:(b + 1) * n])
+
     for _ in range(args.warmup):
         step()
     times = [step() for _ in range(args.steps)]
@@ -223,12 +263,14 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic (repo generator, seed 1002)",
         "impl": "reference",
-        "config": {"workload": f"{cfg.name}: {cfg.frames}x{cfg.height}x{cfg.width} uint16 (step sample: first {n} frames), "
-                               f"r={cfg.radius}, patch=21, L={cfg.segment_length}, M={cfg.ref_frames}",
+        "config": {"workload": f"{cfg.name}: {cfg.frames}x{cfg.height}x{cfg.width} uint16 (step sample: one full "
+                               f"{n}-frame block, blocks in turn), r={cfg.radius}, patch=21, L={cfg.segment_length}, "
+                               f"M={cfg.ref_frames}",
                    "threads": threads},
         "cpu_baseline": {"value": fps, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"first {n} frames of {cfg.name} per step; voltseg correct_motion(threads={threads}) "
-                                   f"+ summarize(L={cfg.segment_length})"},
+                         "sample": f"one {n}-frame block of {cfg.name} per step (block (W+i) mod {nblk}); voltseg "
+                                   f"correct_motion(threads={threads}) + summarize(L={cfg.segment_length}); the "
+                                   f"template is each block's first M frames"},
         "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -273,7 +315,6 @@ def run_ours(args):
         torch.cuda.empty_cache()
         t = shard.frames
         runner = distributed.BalancedShardedPreprocessor(cfg.height, cfg.width, scfg)
-        args.no_e2e = True  # the C-ABI host executor runs whole recordings only
     else:
         # weak scaling: rank r owns frames [r*T, (r+1)*T) of an N*T-frame recording
         frames = synth.generate(synth.SynthConfig(**{**cfg.__dict__, "seed": cfg.seed + rank}), dev)
@@ -388,7 +429,46 @@ def run_ours(args):
 
     # ---- e2e through the C-ABI host entry point ----
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and strong:
+        # each rank streams its own shard over its own PCIe link: pinned host
+        # frames -> HBM, the sharded stage (template all-reduce, straddling
+        # blocks over peer memory), vectors + owned summaries -> pinned host
+        host = frames.view(torch.int16).cpu().pin_memory()
+        dev_in = torch.empty_like(frames)
+        nrec = _lib.MOTION_DTYPE.itemsize * frames.shape[0]
+        kb = shard.block_hi - shard.block_lo
+        vec_h = torch.empty(nrec, dtype=torch.uint8, pin_memory=True)
+        sp_h = torch.empty((max(kb, 1), cfg.height, cfg.width), dtype=torch.float32, pin_memory=True)
+        tp_h = torch.empty_like(sp_h)
+
+        def e2e_step():
+            dev_in.view(torch.int16).copy_(host, non_blocking=True)
+            r = runner.run(dev_in, shard, cfg.ref_frames, corrected_out=corr)
+            vec_h.copy_(r.vectors[:nrec], non_blocking=True)
+            if kb:
+                sp_h[:kb].copy_(r.spatial, non_blocking=True)
+                tp_h[:kb].copy_(r.temporal, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        for _ in range(max(args.warmup, 1)):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        w0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        et = torch.tensor([time.perf_counter() - w0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        hw = cfg.height * cfg.width
+        e2e = {"value": shard.n_total * args.steps / float(et.item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(frames.shape[0] * hw * 2), "d2h_bytes_per_step": int(nrec + 2 * kb * hw * 4),
+               "path": "per rank: pinned uint16 shard (+ halo) -> HBM, sharded stage, vectors + owned summaries -> "
+                       "pinned host; rank 0's bytes; max over ranks"}
+        del host, dev_in
+    elif not args.no_e2e:
         host = frames.view(torch.int16).cpu().pin_memory()
         hs = stage.HostStage(cfg.height, cfg.width, scfg, device=local_dev)
         k = math.ceil(t / cfg.segment_length)
@@ -437,6 +517,40 @@ def run_ours(args):
         hs.close()
         del host
 
+    # ---- e2e through the drop-in Python API, corrected video returned ----
+    dropin = None
+    if not args.no_dropin and not strong:
+        from paper_2403_16438_b200 import Video
+
+        host_np = frames.view(torch.int16).cpu().numpy().view(np.uint16)  # plain (pageable) numpy recording
+        hw = cfg.height * cfg.width
+        k = math.ceil(t / cfg.segment_length)
+
+        def dropin_step():
+            corrected, vectors, pairs = stage.preprocess(Video(host_np), scfg, return_corrected=True)
+            assert corrected.data.shape == (t, cfg.height, cfg.width) and len(vectors) == t and len(pairs) == k
+            del corrected, vectors, pairs  # the caller drops the step's outputs (the pool block is reused)
+
+        for _ in range(max(args.warmup, 1)):
+            dropin_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        w0 = time.perf_counter()
+        for _ in range(args.steps):
+            dropin_step()
+        torch.cuda.synchronize()
+        et = torch.tensor([time.perf_counter() - w0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        dropin = {"value": t * world * args.steps / float(et.item()), "unit": UNIT,
+                  "h2d_bytes_per_step": int(t * hw * 2), "d2h_bytes_per_step": int(t * hw * 4 + t * 32 + 2 * k * hw * 4),
+                  "path": "stage.preprocess(Video(numpy uint16), StageConfig, return_corrected=True): pageable numpy "
+                          "recording in; corrected float32 video (page-locked pool array, direct D2H), "
+                          "MotionVector list and SummaryPair list out -- correct_motion + summarize's return values"}
+        stage.release_cached()
+        del host_np
+
     # ---- CPU baseline: the reference on this host's cores (rank 0, N=1 only) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -455,7 +569,7 @@ def run_ours(args):
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "impl": "ours", "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f32/f64",
             "data": f"synthetic (paper_2403_16438_b200.synth, BASELINE.json configs[1], seed {cfg.seed}"
@@ -464,14 +578,18 @@ def run_ours(args):
                                     f"shards" if strong else f"{cfg.name}: {t}x{cfg.height}x{cfg.width} uint16 per rank")
                                    + f", r={cfg.radius}, patch=21, L={cfg.segment_length}, M={cfg.ref_frames}, sigma=3",
                        "per_rank_frames": t,
+                       "straddling_blocks": (sum(distributed.balanced_plan(total_frames, cfg.segment_length, world, q)
+                                                 .tail is not None for q in range(world)) if strong else 0),
                        "parallelism": (f"frame-balanced time shards x{world} (template all-reduce; straddling blocks: "
-                                       f"smoothed frames + float64 running sum sent forward, NCCL p2p)") if strong
+                                       f"smoothed frames + float64 running sum written into the owner's HBM over "
+                                       f"peer memory)") if strong
                        else f"time-sharded x{world} (template all-reduce)",
                        "corrected_video": "written to HBM" if corr is not None else "not materialised",
                        "l2": "inputs (%.1f GB u16) larger than L2 (126 MB); no flush" % (t * cfg.height * cfg.width * 2 / 1e9)},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_dropin": dropin,
             "gpu_launches": int(launches),
             "clocks": clk,
             "outputs_sane": ok,
@@ -642,6 +760,14 @@ def run_pipeline(args):
 
 def main():
     args = parse()
+    rc = relaunch_under_torchrun(args)
+    if rc is not None:
+        return rc
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.scaling is None:
+        args.scaling = "strong" if world > 1 else "weak"
     if args.stage == "unet":
         return run_unet(args)
     if args.stage == "pipeline":

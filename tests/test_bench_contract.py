@@ -40,6 +40,30 @@ def test_our_arm_contract():
     r = d["roofline"]
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(r) and 0 < r["frac"] < 1
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["gpu_launches"] > 0 and d["outputs_sane"]
+    assert d["impl"] == "ours" and d["e2e_dropin"]["value"] > 0
+    assert d["e2e_dropin"]["d2h_bytes_per_step"] > 600 * 128 * 128 * 4  # the corrected video comes back
+
+
+@pytest.mark.gpu
+def test_gpus_2_runs_two_ranks_with_exchange():
+    """`bench.py --gpus 2` outside torchrun re-launches itself as two ranks
+    (strong scaling, frame-balanced shards, one straddling block exchanged
+    over peer memory).  On a one-GPU box both ranks share the device and the
+    collectives run over gloo (host-mediated: no kernel waits on another
+    rank's kernel); the measured configuration uses NCCL."""
+    import os
+
+    env = dict(os.environ, BENCH_DIST_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--config", "c1", "--frames", "700",
+                          "--steps", "2", "--warmup", "3", "--no-cpu-baseline"], capture_output=True, text=True,
+                         timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["config"]["straddling_blocks"] == 1
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["outputs_sane"]
 
 
 @pytest.mark.gpu
