@@ -74,6 +74,56 @@ def test_oracle_shading_gain_properties(oracle_mod, rng):
     assert g[32, 40] > g[0, 0]
 
 
+# ---------------------------------------------------------------- CPU: pinned to scipy
+# The A17 definitions restated with scipy's published filters (scipy 1.18.1,
+# the reference's pinned dependency, pyproject.toml:11-12): the shading gain is
+# gaussian_filter(template, sigma, mode="reflect", truncate=4) / its mean, the
+# high-pass is x - uniform_filter1d(x, N, axis=0, mode="reflect") on the
+# reference's smoothed stack (summarize.py:70-73), then the reference's
+# max - median (summarize.py:76-92).  Tolerance: 1e-4 relative (the north
+# star's float32 bound; the two differ only in float64 summation order and
+# where the float32 rounding happens).
+def scipy_shading_gain(ref, sigma):
+    from scipy import ndimage
+
+    g = ndimage.gaussian_filter(np.asarray(ref, np.float64), sigma, mode="reflect", truncate=4.0)
+    return (g / g.mean()).astype(np.float32)
+
+
+def scipy_highpass_summary(frames, L, window, sigma=3.0):
+    from scipy import ndimage
+
+    f = np.asarray(frames, np.float32)
+    sm = ndimage.gaussian_filter1d(f, sigma, axis=1, mode="reflect", radius=9)
+    sm = ndimage.gaussian_filter1d(sm, sigma, axis=2, mode="reflect", radius=9)
+    s64 = sm.astype(np.float64)
+    hp = (s64 - ndimage.uniform_filter1d(s64, window, axis=0, mode="reflect")).astype(np.float32)
+    out = []
+    for b0 in range(0, f.shape[0], L):
+        blk = hp[b0:b0 + L]
+        o = np.sort(blk, axis=0)
+        n, mid = blk.shape[0], blk.shape[0] // 2
+        med = o[mid] if n % 2 else (o[mid - 1] + o[mid]) * np.float32(0.5)
+        out.append(blk.max(axis=0) - med)
+    return np.stack(out)
+
+
+@pytest.mark.parametrize("shape,sigma", [((96, 128), 16.0), ((33, 70), 40.0), ((64, 80), 4.0)])
+def test_oracle_shading_gain_vs_scipy(oracle_mod, shape, sigma):
+    rng = np.random.default_rng(3)
+    ref = (1000.0 + 300.0 * rng.random(shape)).astype(np.float32)
+    np.testing.assert_allclose(oracle_mod.shading_gain(ref, sigma), scipy_shading_gain(ref, sigma), rtol=1e-6)
+
+
+@pytest.mark.parametrize("shape,L,win", [((300, 40, 72), 100, 33), ((122, 30, 40), 40, 3), ((20, 24, 24), 10, 33)])
+def test_oracle_highpass_vs_scipy(oracle_mod, shape, L, win):
+    frames = _frames(shape)
+    got = oracle_mod.highpass_summary(frames, L, win)
+    want = scipy_highpass_summary(frames, L, win)
+    assert np.abs(got - want).max() <= 1e-4 * np.abs(frames).max()
+    np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-4 * np.abs(frames).max())
+
+
 # ---------------------------------------------------------------- GPU
 def _frames(shape, seed=7):
     rng = np.random.default_rng(seed)
@@ -240,3 +290,26 @@ def test_highpass_one_frame_tail_raises_like_reference(cuda):
     frames = _frames((121, 30, 40))
     with pytest.raises(ValueError, match="at least 2 frames"):
         summarize(frames, 40, highpass_window=3)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,sigma", [((96, 128), 16.0), ((256, 512), 32.0), ((33, 70), 40.0)])
+def test_shading_gain_vs_scipy(cuda, shape, sigma):
+    """A17 shading gain on the CUDA path against scipy.ndimage.gaussian_filter."""
+    rng = np.random.default_rng(11)
+    ref = (1000.0 + 300.0 * rng.random(shape)).astype(np.float32)
+    np.testing.assert_allclose(extensions.shading_gain(ref, sigma), scipy_shading_gain(ref, sigma), rtol=1e-4)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,L,win", [((300, 40, 72), 100, 33), ((250, 33, 70), 64, 9), ((20, 24, 24), 10, 33)])
+def test_highpass_summary_vs_scipy(cuda, shape, L, win):
+    """A17 high-passed temporal summary on the CUDA path against
+    x - scipy.ndimage.uniform_filter1d(x, N, axis=0, mode="reflect") of the
+    reference's smoothed stack, then max - median, within 1e-4."""
+    from paper_2403_16438_b200.summarize import summarize
+
+    frames = _frames(shape)
+    got = np.stack([p.temporal for p in summarize(frames, L, highpass_window=win)])
+    want = scipy_highpass_summary(frames, L, win)
+    np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-4 * np.abs(frames).max())
