@@ -112,6 +112,7 @@ def scipy_highpass_summary(frames, L, window, sigma=3.0):
 def test_oracle_shading_gain_vs_scipy(oracle_mod, shape, sigma):
     rng = np.random.default_rng(3)
     ref = (1000.0 + 300.0 * rng.random(shape)).astype(np.float32)
+    # measured bit-identical on these inputs (held to 1e-6 relative)
     np.testing.assert_allclose(oracle_mod.shading_gain(ref, sigma), scipy_shading_gain(ref, sigma), rtol=1e-6)
 
 
@@ -120,8 +121,7 @@ def test_oracle_highpass_vs_scipy(oracle_mod, shape, L, win):
     frames = _frames(shape)
     got = oracle_mod.highpass_summary(frames, L, win)
     want = scipy_highpass_summary(frames, L, win)
-    assert np.abs(got - want).max() <= 1e-4 * np.abs(frames).max()
-    np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-4 * np.abs(frames).max())
+    np.testing.assert_array_equal(got, want)  # bit-identical: same float64 sums, same rounding points
 
 
 # ---------------------------------------------------------------- GPU
