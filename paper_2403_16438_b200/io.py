@@ -8,9 +8,10 @@ format, half the bytes over disk/PCIe) and reads files through `np.memmap`,
 so `preprocess_file` streams a recording straight from the page cache into
 the C-ABI stage executor (`vb_stage_run_host` packs pageable chunks into its
 pinned ring) without ever holding the whole video in host RAM -- the
-long-recording case (BASELINE configs[3]: 100,000 x 512 x 512).  TIFF is
-read/written through `tifffile` when it is installed (it is not in this
-image); a missing package raises VideoIOError like a bad file does.
+long-recording case (BASELINE configs[3]: 100,000 x 512 x 512).  Multi-page
+TIFF is read and written by the in-repo reader (tiff.py; the reference uses
+`tifffile`, absent from this image), memory-mapped when the pages' data are
+contiguous, so TIFF recordings stream into the executor the same way.
 """
 from __future__ import annotations
 
@@ -19,6 +20,7 @@ from pathlib import Path
 
 import numpy as np
 
+from .tiff import TiffError, read_tiff, write_tiff
 from .video import Video
 
 VSEGV_MAGIC = b"VSEGV1\0\0"
@@ -71,17 +73,33 @@ def load_video(path: str | Path) -> Video:
     if is_raw:
         arr, rate = open_raw(path)
         return Video(np.array(arr), frame_rate=rate)
+    return Video(np.array(_open_tiff(path)))
+
+
+def _open_tiff(path: Path) -> np.ndarray:
+    """video_io.py:98-126 error mapping over the in-repo TIFF reader."""
     try:
-        import tifffile
-    except ImportError as exc:
-        raise VideoIOError(f"{path}: TIFF input needs the tifffile package") from exc
-    try:
-        data = tifffile.imread(path)
+        return read_tiff(path)
+    except TiffError as exc:
+        msg = str(exc)
+        raise VideoIOError(msg if msg.startswith(str(path)) else f"{path}: unreadable TIFF: {msg}") from exc
     except Exception as exc:  # noqa: BLE001 - mirror the reference's error mapping
         raise VideoIOError(f"{path}: unreadable TIFF: {exc}") from exc
-    if data.ndim == 2:
-        data = data[None]
-    return Video(data)
+
+
+def open_recording(path: str | Path) -> np.ndarray:
+    """(T, H, W) uint16/float32 (uint8 widened) view of a VSEGV1 or TIFF file,
+    memory-mapped where the layout allows: the executor streams it from the
+    page cache."""
+    path = Path(path)
+    if not path.is_file():
+        raise VideoIOError(f"cannot read video file: {path}")
+    with open(path, "rb") as f:
+        is_raw = f.read(8) == VSEGV_MAGIC
+    if is_raw:
+        return open_raw(path)[0]
+    arr = _open_tiff(path)
+    return arr if arr.dtype in (np.uint16, np.float32) else arr.astype(np.float32)
 
 
 def save_video(video, path: str | Path, sample: str = "auto") -> None:
@@ -93,11 +111,13 @@ def save_video(video, path: str | Path, sample: str = "auto") -> None:
     if str(path) == "":
         raise VideoIOError("empty output path")
     if path.suffix != ".vsegv1":
+        # the reference writes the float32 data as a minisblack multi-page TIFF
+        # (video_io.py:154-157); sample="u16" keeps the camera counts
+        data = v.raw if (sample == "u16" and v.raw is not None) else v.data
         try:
-            import tifffile
-        except ImportError as exc:
-            raise VideoIOError(f"cannot write {path}: tifffile is not installed") from exc
-        tifffile.imwrite(path, v.data, photometric="minisblack")
+            write_tiff(path, data)
+        except Exception as exc:  # noqa: BLE001
+            raise VideoIOError(f"cannot write {path}: {exc}") from exc
         return
     use_u16 = sample == "u16" or (sample == "auto" and v.raw is not None)
     fmt = SAMPLE_U16 if use_u16 else SAMPLE_F32
@@ -113,14 +133,14 @@ def save_video(video, path: str | Path, sample: str = "auto") -> None:
 
 
 def preprocess_file(path: str | Path, config=None, device: int | None = None, chunk_frames: int = 0):
-    """Stream a VSEGV1 recording from disk through the C-ABI stage executor.
+    """Stream a VSEGV1 or TIFF recording from disk through the C-ABI stage executor.
 
     Returns (vectors record array, spatial [K,H,W], temporal [K,H,W]); the
     corrected video is formed on the fly in HBM only."""
     from . import _lib
     from .stage import HostStage
 
-    arr, _rate = open_raw(path)
+    arr = open_recording(path)
     t, h, w = arr.shape
     hs = HostStage(h, w, config, device=device, chunk_frames=chunk_frames)
     try:

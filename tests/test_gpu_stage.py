@@ -248,14 +248,15 @@ def test_streamed_long_recording_c4_geometry(cuda):
 
 
 @pytest.mark.parametrize("sample", ["u16", "f32"])
-def test_preprocess_file_streams_from_disk(cuda, tmp_path, c1_small, sample):
-    """configs[3]-style ingest: memory-mapped VSEGV1 file -> C-ABI executor,
-    identical to the in-memory run."""
+@pytest.mark.parametrize("ext", [".vsegv1", ".tif"])
+def test_preprocess_file_streams_from_disk(cuda, tmp_path, c1_small, sample, ext):
+    """configs[3]-style ingest: memory-mapped VSEGV1 or TIFF file -> C-ABI
+    executor, identical to the in-memory run."""
     from paper_2403_16438_b200 import io
     cfg, raw = c1_small
     sc = _stage_cfg(cfg, 100)
-    io.save_video(Video(raw, frame_rate=741.0), tmp_path / "r.vsegv1", sample=sample)
-    vec, sp, tp = io.preprocess_file(tmp_path / "r.vsegv1", sc, chunk_frames=100)
+    io.save_video(Video(raw, frame_rate=741.0), tmp_path / f"r{ext}", sample=sample)
+    vec, sp, tp = io.preprocess_file(tmp_path / f"r{ext}", sc, chunk_frames=100)
     _, vectors, pairs = preprocess(Video(raw), sc)
     np.testing.assert_array_equal(vec["dx"], [v.dx for v in vectors])
     np.testing.assert_array_equal(vec["sub_dy"], [v.sub_dy for v in vectors])
