@@ -293,6 +293,26 @@ int vb_stage_run_host_segment(vb_stage* stage, const void* frames_host, int dtyp
                               vb_motion* vectors_host, float* spatial_host, float* temporal_host, float* prob_host,
                               float* corrected_host, float* corrected_dev);
 
+/* ---------------- several GPUs from one process (no torch.distributed) ----------------
+ * a group of devices, one vb_stage per device and
+ * one NCCL communicator per device (ncclCommInitAll; NCCL is dlopen'ed).  The
+ * recording is split into block-aligned time shards (vb_group_plan: whole
+ * L-frame blocks, as evenly as possible), the template is the float64 sum of
+ * the first min(n, ref_frames) frames all-reduced over NCCL (each device sums
+ * its own frames of that range; every device divides identically), and each
+ * device then streams its shard through its executor in its own host thread.
+ * Outputs land in the caller's buffers exactly as vb_stage_run_host's would
+ * for the whole recording on one device (bit-identical). */
+typedef struct vb_group vb_group;
+/* frame_bounds[n_devices + 1]: shard d = frames [frame_bounds[d], frame_bounds[d+1]). */
+int vb_group_plan(int64_t n_frames, int segment_length, int n_devices, int64_t* frame_bounds);
+int vb_group_create(vb_group** group, const int* devices, int n_devices, const vb_stage_config* cfg);
+int vb_group_set_weights(vb_group* group, const double* weights, int wradius);
+int vb_group_run_host(vb_group* group, const void* frames_host, int dtype, int64_t n_frames,
+                      vb_motion* vectors_host, float* spatial_host, float* temporal_host, float* corrected_host);
+int64_t vb_group_last_launches(const vb_group* group);
+int vb_group_destroy(vb_group* group);
+
 /* Page-locked host memory (cudaHostAlloc, portable).  A corrected_host
  * buffer passed to vb_stage_run_host that is page-locked (from here or
  * cudaHostRegister) receives each chunk by a direct device->host copy; a

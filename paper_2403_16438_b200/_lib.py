@@ -92,6 +92,12 @@ SIGNATURES = {
     "vb_stage_run_host_segment": (_i32, [_vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "vb_stage_destroy": (_i32, [_vp]),
     "vb_stage_set_reference": (_i32, [_vp, _vp]),
+    "vb_group_plan": (_i32, [_i64, _i32, _i32, _vp]),
+    "vb_group_create": (_i32, [C.POINTER(_vp), _vp, _i32, C.POINTER(VbStageConfig)]),
+    "vb_group_set_weights": (_i32, [_vp, _vp, _i32]),
+    "vb_group_run_host": (_i32, [_vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp]),
+    "vb_group_last_launches": (_i64, [_vp]),
+    "vb_group_destroy": (_i32, [_vp]),
     "vb_host_alloc": (_i32, [_i64, C.POINTER(_vp)]),
     "vb_host_free": (_i32, [_vp]),
     "vb_host_copy": (_i32, [_vp, _vp, _i64, _i32]),

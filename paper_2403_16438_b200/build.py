@@ -13,7 +13,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libvoltb200.so"
 LIB_EXP = PKG / "libvoltb200_exp.so"  # experiment build (A/B switches live); loaded only via VB_LIBRARY
-SOURCES = ["capi.cu", "stage.cu", "motion.cu", "summary.cu", "probe.cu", "traces.cu", "unet.cu"]
+SOURCES = ["capi.cu", "stage.cu", "group.cu", "motion.cu", "summary.cu", "probe.cu", "traces.cu", "unet.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-O3",
          f"-I{ROOT / 'include'}"]
@@ -63,7 +63,7 @@ def build(force: bool = False, verbose: bool = False, experiments: bool = False)
     if failed:
         raise RuntimeError(f"nvcc failed for {failed}")
     tmp = lib.with_suffix(".so.tmp")
-    subprocess.run([cc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart"], check=True)
+    subprocess.run([cc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart", "-ldl"], check=True)
     os.replace(tmp, lib)
     return lib
 

@@ -986,6 +986,7 @@ size_t zncc_search_smem_bytes(int patch, int radius, int max_g, int max_wu, int 
 int launch_motion(const Templates& t, int h, int w, int patch, int radius, const void* frames, int dtype,
                   int64_t n_frames, int subpixel, vb_motion* vectors, double* scores, cudaStream_t s) {
     if (n_frames <= 0) return VB_OK;
+    NvtxRange nv("motion search");
     const int S = 2 * radius + 1, SS = S * S;
     bool fast = false;
     pick_kernel(patch, S, 1, &fast);

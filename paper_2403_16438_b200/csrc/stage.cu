@@ -319,6 +319,7 @@ static int stage_run(vb_stage* st, const void* frames_host, int dtype, int64_t n
                      float* corrected_dev) {
     if (!st || !frames_host || !vectors_host) return fail(VB_EINVAL, "null argument");
     const int64_t launches0 = launches().load();
+    NvtxRange nv("vb_stage_run_host");
     int rc = stage_run_impl(st, frames_host, dtype, n_frames, vectors_host, spatial_host, temporal_host, prob_host,
                             corrected_host, corrected_dev);
     const cudaError_t e = (cudaError_t)stage_sync_all(st);
@@ -408,6 +409,7 @@ static int stage_run_impl(vb_stage* st, const void* frames_host, int dtype, int6
     auto part = [&](int64_t nf, int j) { return nf * j / nparts(nf); };
     // host->device copy of frames [f0, f0+nf) into slot, piece by piece
     auto upload = [&](int slot, int64_t f0, int64_t nf) -> int {
+        NvtxRange nv_up("upload");
         if (!pinned) VB_CUDA(cudaEventSynchronize(st->ev_h2d[slot]));  // staging slot free again
         VB_CUDA(cudaStreamWaitEvent(st->s_h2d, st->ev_comp[slot], 0));  // slot no longer read by compute
         for (int j = 0; j < nparts(nf); ++j) {
@@ -472,6 +474,7 @@ static int stage_run_impl(vb_stage* st, const void* frames_host, int dtype, int6
         const int slot = (int)(k & 1);
         const int64_t f0 = k * C, nf = std::min<int64_t>(C, n_frames - f0);
         const int64_t b0 = f0 / L, nb = (nf + L - 1) / L;
+        NvtxRange nv_dr("drain");
         VB_CUDA(cudaEventSynchronize(st->ev_d2h[slot]));
         memcpy(vectors_host + f0, st->h_vec[slot], (size_t)nf * sizeof(vb_motion));
         if (!motion_only) {
@@ -484,6 +487,7 @@ static int stage_run_impl(vb_stage* st, const void* frames_host, int dtype, int6
         return VB_OK;
     };
     for (int64_t k = 0; k < nchunks && rc == VB_OK; ++k) {
+        NvtxRange nv_chunk("chunk " + std::to_string(k));
         const int slot = (int)(k & 1);
         const int64_t f0 = k * C, nf = std::min<int64_t>(C, n_frames - f0);
         const int64_t nb = (nf + L - 1) / L;

@@ -5,6 +5,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <atomic>
 #include <string>
 
@@ -44,6 +46,15 @@ inline int knob(const char* name, int dflt) {
         cudaError_t e_ = cudaGetLastError();                               \
         if (e_ != cudaSuccess) return ::vb::cuda_fail(e_, "kernel launch"); \
     } while (0)
+
+// ---- NVTX ranges (host timeline for nsys / ncu --nvtx; no-ops without a tool)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    explicit NvtxRange(const std::string& name) { nvtxRangePushA(name.c_str()); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // ---- per-kernel CUDA-event profiler (vb_prof_enable / vb_prof_collect) ----
 enum KernelId { kProfZncc = 0, kProfFinalize = 1, kProfWarpSmooth = 2, kProfMedian = 3, kProfOther = 4,

@@ -401,3 +401,64 @@ class HostStage:
             self.close()
         except Exception:
             pass
+
+
+def group_plan(n_frames: int, segment_length: int, n_devices: int) -> list[tuple[int, int]]:
+    """Block-aligned shards of vb_group (frames [lo, hi) per device)."""
+    b = np.empty(n_devices + 1, np.int64)
+    _lib.call("vb_group_plan", int(n_frames), int(segment_length), int(n_devices), b.ctypes.data)
+    return [(int(b[i]), int(b[i + 1])) for i in range(n_devices)]
+
+
+class GroupStage:
+    """vb_group: several GPUs driven from one process through the C ABI alone
+     -- block-aligned time shards, the template all-reduced
+    over NCCL inside the library, one executor per device.  Outputs equal a
+    single-device HostStage run of the whole recording."""
+
+    def __init__(self, height: int, width: int, config: StageConfig | None = None, devices=(0,)):
+        c = _resolved(config)
+        self.cfg = c
+        devs = np.ascontiguousarray(list(devices), dtype=np.int32)
+        sc = _lib.VbStageConfig(height, width, c.patch_size, c.search_radius, int(c.subpixel), c.ref_frames,
+                                c.segment_length, float(c.sigma), int(devs[0]), 0)
+        if c.highpass_window or c.shading_sigma:
+            raise ValueError("the device group runs the reference stage only (no A17 options)")
+        h = C.c_void_p()
+        _lib.call("vb_group_create", C.byref(h), devs.ctypes.data, len(devs), C.byref(sc))
+        self._h = h
+        w, r = gaussian_weights(c.sigma)
+        self._w = w
+        _lib.call("vb_group_set_weights", self._h, w.ctypes.data, r)
+        self.height, self.width, self.devices = height, width, tuple(int(d) for d in devs)
+
+    def run(self, frames: np.ndarray, corrected: bool = False):
+        a = np.ascontiguousarray(frames)
+        if a.dtype not in (np.uint16, np.float32):
+            a = a.astype(np.float32)
+        dtype = _lib.VB_U16 if a.dtype == np.uint16 else _lib.VB_F32
+        t = a.shape[0]
+        k = math.ceil(t / self.cfg.segment_length)
+        vec = np.empty(t, dtype=_lib.MOTION_DTYPE)
+        sp = np.empty((k, self.height, self.width), np.float32)
+        tp = np.empty_like(sp)
+        corr = pinned_empty((t, self.height, self.width)) if corrected else None
+        _lib.call("vb_group_run_host", self._h, a.ctypes.data, dtype, t, vec.ctypes.data, sp.ctypes.data,
+                  tp.ctypes.data, corr.ctypes.data if corr is not None else None)
+        return vec, sp, tp, corr
+
+    @property
+    def last_launches(self) -> int:
+        return int(_lib.load().vb_group_last_launches(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None) is not None:
+            _lib.load().vb_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+

@@ -335,3 +335,31 @@ def test_corrected_output_pinned_pool_and_out(cuda, c1_small):
     with pytest.raises(ValueError, match="out must be"):
         preprocess(Video(raw), sc, out=np.empty((1, 2, 3), np.float32))
     stage.release_cached()
+
+
+def test_device_group_equals_single_device(cuda, c1_small):
+    """vb_group (C-ABI multi-device handle, NCCL template all-reduce inside the
+    library) on every visible GPU == the single-device executor, bit for bit.
+    On a one-GPU box the group has one member (ncclCommInitAll over one
+    device, the all-reduce is the identity); the shard split itself is
+    host-tested in test_host_logic.py."""
+    from paper_2403_16438_b200.stage import GroupStage
+
+    cfg, raw = c1_small
+    sc = _stage_cfg(cfg, 100)
+    devices = list(range(torch.cuda.device_count()))
+    g = GroupStage(raw.shape[1], raw.shape[2], sc, devices=devices)
+    try:
+        vec, sp, tp, corr = g.run(raw, corrected=True)
+        assert g.last_launches > 0
+    finally:
+        g.close()
+    hs = HostStage(raw.shape[1], raw.shape[2], sc)
+    try:
+        v2, s2, t2, c2 = hs.run(raw, corrected=True)
+    finally:
+        hs.close()
+    np.testing.assert_array_equal(vec, v2)
+    np.testing.assert_array_equal(sp, s2)
+    np.testing.assert_array_equal(tp, t2)
+    np.testing.assert_array_equal(corr, c2)

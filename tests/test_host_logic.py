@@ -192,3 +192,19 @@ class TestShardPlan:
         assert distributed.template_rows(s1, 100) == (0, 0)
         s2 = distributed.shard_plan(150, 50, 3, 1)  # frames 50..100 hold template rows 50..99
         assert distributed.template_rows(s2, 100) == (0, 50)
+
+
+def test_group_plan_block_aligned():
+    """vb_group_plan (C ABI, host only): whole blocks per device, as even as
+    possible, covering the recording (distributed.shard_plan's split)."""
+    from paper_2403_16438_b200 import distributed
+    from paper_2403_16438_b200.stage import group_plan
+
+    for t, L, n in [(10000, 1000, 8), (10000, 1000, 3), (2500, 1000, 4), (7, 2, 5), (1000, 500, 1)]:
+        plan = group_plan(t, L, n)
+        assert plan[0][0] == 0 and plan[-1][1] == t
+        for (a, b), (c, _d) in zip(plan, plan[1:]):
+            assert b == c and (a % L == 0 or a == t)
+        for r in range(n):
+            s = distributed.shard_plan(t, L, n, r)
+            assert plan[r] == (s.frame_lo, s.frame_hi)
