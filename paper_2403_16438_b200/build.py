@@ -13,7 +13,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libvoltb200.so"
 LIB_EXP = PKG / "libvoltb200_exp.so"  # experiment build (A/B switches live); loaded only via VB_LIBRARY
-SOURCES = ["capi.cu", "stage.cu", "group.cu", "motion.cu", "summary.cu", "probe.cu", "traces.cu", "unet.cu"]
+SOURCES = ["capi.cu", "stage.cu", "group.cu", "motion.cu", "zncc_mma.cu", "summary.cu", "probe.cu", "traces.cu", "unet.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-O3",
          f"-I{ROOT / 'include'}"]
@@ -30,7 +30,7 @@ def _stale(lib: Path = LIB) -> bool:
     if not lib.exists():
         return True
     t = lib.stat().st_mtime
-    deps = [CSRC / s for s in SOURCES] + [CSRC / "vb.cuh", ROOT / "include" / "voltb200.h"]
+    deps = [CSRC / s for s in SOURCES] + [CSRC / "vb.cuh", CSRC / "tma.cuh", ROOT / "include" / "voltb200.h"]
     return any(d.stat().st_mtime > t for d in deps)
 
 

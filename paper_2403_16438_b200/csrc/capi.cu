@@ -19,7 +19,8 @@
 namespace vb {
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point.
-bool make_frames_tmap(CUtensorMap* map, const void* base, int dtype, int64_t t, int h, int w, int bh, int bw) {
+bool make_frames_tmap(CUtensorMap* map, const void* base, int dtype, int64_t t, int h, int w, int bh, int bw,
+                      int bt) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     static bool tried = false;
     if (!tried) {
@@ -34,10 +35,10 @@ bool make_frames_tmap(CUtensorMap* map, const void* base, int dtype, int64_t t, 
     if (!encode || !base) return false;
     const size_t esz = dtype == VB_U16 ? 2 : 4;
     if ((reinterpret_cast<uintptr_t>(base) & 15) || ((size_t)w * esz) % 16 || ((size_t)h * w * esz) % 16) return false;
-    if (bw < 1 || bh < 1 || bw > 256 || bh > 256 || ((size_t)bw * esz) % 16) return false;
+    if (bw < 1 || bh < 1 || bt < 1 || bw > 256 || bh > 256 || bt > 256 || ((size_t)bw * esz) % 16) return false;
     cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)(t > 0 ? t : 1)};
     cuuint64_t strides[2] = {(cuuint64_t)(w * esz), (cuuint64_t)((size_t)h * w * esz)};
-    cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, 1};
+    cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bt};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = encode(map, dtype == VB_U16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                         const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -111,6 +112,10 @@ struct vb_motion_plan {
 };
 
 static void free_templates(Templates& t) {
+    cudaFree(t.t16);
+    cudaFree(t.tscale);
+    cudaFree(t.cen);
+    cudaFree(t.patch_group);
     cudaFree(t.tmpl);
     cudaFree(t.rvar);
     cudaFree(t.origins);
@@ -366,6 +371,17 @@ int vb_motion_plan_create(vb_motion_plan** out, int height, int width, int patch
     e = e ? e : cudaMemcpy(t.origins, origins_host, (size_t)n_origins * 2 * sizeof(int32_t), cudaMemcpyHostToDevice);
     e = e ? e : cudaMemcpy(t.patch_col, col.data(), col.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
     e = e ? e : cudaMemcpy(t.groups, groups.data(), groups.size() * sizeof(PatchGroup), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && mma_supported(patch, radius, VB_U16)) {  // tensor-core path tables (uint16 frames)
+        const MmaGeom g = mma_geom(patch, radius);
+        std::vector<int32_t> pg(n_origins);
+        for (size_t gi = 0; gi < groups.size(); ++gi)
+            for (int q = 0; q < groups[gi].count; ++q) pg[groups[gi].first + q] = (int32_t)gi;
+        e = e ? e : cudaMalloc(&t.t16, (size_t)n_origins * 8 * 2 * patch * g.tpw * 2);
+        e = e ? e : cudaMalloc(&t.tscale, (size_t)n_origins * sizeof(float));
+        e = e ? e : cudaMalloc(&t.cen, (size_t)n_origins * sizeof(int32_t));
+        e = e ? e : cudaMalloc(&t.patch_group, (size_t)n_origins * sizeof(int32_t));
+        e = e ? e : cudaMemcpy(t.patch_group, pg.data(), pg.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+    }
     if (e != cudaSuccess) {
         free_templates(t);
         delete p;
@@ -378,6 +394,7 @@ int vb_motion_plan_create(vb_motion_plan** out, int height, int width, int patch
 int vb_motion_plan_set_reference(vb_motion_plan* p, const float* ref_dev, void* stream) {
     if (!p || !ref_dev) return fail(VB_EINVAL, "null argument");
     int rc = launch_prep_templates(ref_dev, p->h, p->w, p->patch, p->t, (cudaStream_t)stream);
+    if (rc == VB_OK && p->t.t16) rc = launch_mma_prep(p->t, p->patch, p->radius, (cudaStream_t)stream);
     if (rc == VB_OK) p->have_ref = true;
     return rc;
 }

@@ -137,6 +137,8 @@ struct ZnccArgs {
     int64_t n_frames;
     float* inv;       // [n_frames][N][S*S]  1/sqrt(fvar*rvar) (0 where the reference skips)
     double* partial;  // [n_frames][n_groups][S*S]
+    const float* cov; // COMBINE statistics: [n_frames][N][ss_pad] cross sums from zncc_mma_kernel
+    int off_sinv;     // COMBINE statistics: shared [G][ss_pad] inv rows
 };
 
 constexpr int kGenericDXB = 8;
@@ -235,7 +237,11 @@ __device__ __forceinline__ void store_row(float* out, const float (&v)[S]) {
     for (int i = head + 4 * nv; i < S; ++i) out[i] = v[i];
 }
 
-template <bool INT, int P_CT, int S_CT = 0>
+// COMBINE (tensor-core path): the inv rows stay in shared memory and the
+// kernel finishes the search -- partial[t][group][c] = sum over the group's
+// patches q (in order) of cov[t][q][c] * inv[q][c] in float64, the cross sums
+// coming from zncc_mma_kernel (no inv round trip through HBM).
+template <bool INT, int P_CT, int S_CT = 0, bool COMBINE = false>
 __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __grid_constant__ CUtensorMap tmap) {
     using T1 = typename std::conditional<INT, int, double>::type;        // sample / sum of f
     using T2 = typename std::conditional<INT, long long, double>::type;  // sum of f^2
@@ -339,7 +345,8 @@ __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __gri
                     h2 += r2[xx];
                 }
             }
-            float* out = a.inv + ((size_t)t * a.n_patches + gp) * a.ss_pad + (size_t)dy * S;
+            float* out = COMBINE ? reinterpret_cast<float*>(smem + a.off_sinv) + (size_t)p * a.ss_pad + (size_t)dy * S
+                                 : a.inv + ((size_t)t * a.n_patches + gp) * a.ss_pad + (size_t)dy * S;
             float ivs[S_CT ? S_CT : 1];
 #pragma unroll
             for (int dx = 0; dx < (S_CT ? S_CT : 64); ++dx) {
@@ -371,12 +378,29 @@ __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __gri
                 }
             }
             if constexpr (S_CT != 0) {
-                switch ((dy * S_CT) & 3) {  // warp-uniform except where two phases meet
-                    case 0: store_row<S_CT, 0>(out, ivs); break;
-                    case 1: store_row<S_CT, 1>(out, ivs); break;
-                    case 2: store_row<S_CT, 2>(out, ivs); break;
-                    default: store_row<S_CT, 3>(out, ivs); break;
+                if constexpr (COMBINE) {
+#pragma unroll
+                    for (int dx = 0; dx < S_CT; ++dx) out[dx] = ivs[dx];
+                } else {
+                    switch ((dy * S_CT) & 3) {  // warp-uniform except where two phases meet
+                        case 0: store_row<S_CT, 0>(out, ivs); break;
+                        case 1: store_row<S_CT, 1>(out, ivs); break;
+                        case 2: store_row<S_CT, 2>(out, ivs); break;
+                        default: store_row<S_CT, 3>(out, ivs); break;
+                    }
                 }
+            }
+        }
+        if constexpr (COMBINE) {
+            __syncthreads();  // the group's inv rows are complete
+            const float* sinv = reinterpret_cast<const float*>(smem + a.off_sinv);
+            const float* cov = a.cov + ((size_t)t * a.n_patches + grp.first) * a.ss_pad;
+            double* part = a.partial + ((size_t)t * a.n_groups + blockIdx.x) * SS;
+            for (int c = threadIdx.x; c < SS; c += blockDim.x) {
+                double acc = 0.0;
+                for (int q = 0; q < G; ++q)
+                    acc = fma((double)__ldg(cov + (size_t)q * a.ss_pad + c), (double)sinv[(size_t)q * a.ss_pad + c], acc);
+                part[c] = acc;
             }
         }
     }
@@ -1028,7 +1052,23 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
         if (S == 25) stats_fn = zncc_stats_kernel<true, 21, 25>;
         if (S == 11) stats_fn = zncc_stats_kernel<true, 21, 11>;
     }
+    // tensor-core cross sums (zncc_mma.cu) + combining statistics kernel, uint16 frames
+    const bool mma = dtype == VB_U16 && t.t16 != nullptr && mma_supported(patch, radius, dtype);
+    if (mma) {
+        stats_fn = zncc_stats_kernel<true, 0, 0, true>;
+        if (patch == 21 && !knob("VB_NO_STATS_S", 0)) {
+            if (S == 17) stats_fn = zncc_stats_kernel<true, 21, 17, true>;
+            if (S == 21) stats_fn = zncc_stats_kernel<true, 21, 21, true>;
+            if (S == 25) stats_fn = zncc_stats_kernel<true, 21, 25, true>;
+            if (S == 11) stats_fn = zncc_stats_kernel<true, 21, 11, true>;
+        } else if (patch == 21) {
+            stats_fn = zncc_stats_kernel<true, 21, 0, true>;
+        }
+    }
     SmemPlan sp = zncc_smem(patch, radius, t.max_g, t.max_wu, dtype, fpi, fast, t.pitch);
+    const int ss_pad_c = (S * S + 3) & ~3;
+    const size_t sinv_off = (sp.stats_total + 15) & ~(size_t)15;
+    if (mma) sp.stats_total = sinv_off + (size_t)t.max_g * ss_pad_c * sizeof(float);
     if (std::max(sp.total, sp.stats_total) > 227 * 1024)
         return fail(VB_EINVAL, "patch group does not fit in shared memory");
     // the search kernel also receives the group's inv rows by bulk copy (fast path, one frame per iteration)
@@ -1040,7 +1080,7 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     const size_t inv_buf = want_inv ? (size_t)fpi * t.max_g * ss_pad_ * sizeof(float) : 0;
     const size_t search_smem = ((sp.total + 15) & ~(size_t)15) + inv_buf;
     if (search_smem > 227 * 1024) return fail(VB_EINVAL, "patch group does not fit in shared memory");
-    VB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)search_smem));
+    if (!mma) VB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)search_smem));
     VB_CUDA(cudaFuncSetAttribute(stats_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.stats_total));
 
     ZnccArgs a;
@@ -1072,6 +1112,15 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     CUtensorMap tmap;
     memset(&tmap, 0, sizeof(tmap));
     a.use_tma = !knob("VB_NO_TMA", 0) && make_frames_tmap(&tmap, frames, dtype, n_frames, h, w, sp.bhc, sp.bw) ? 1 : 0;
+    // tensor-core path: boxes of one window row x 128 frames
+    CUtensorMap tmap_mma;
+    memset(&tmap_mma, 0, sizeof(tmap_mma));
+    const bool use_mma = mma && a.use_tma && make_frames_tmap(&tmap_mma, frames, dtype, n_frames, h, w, 1, 56, 128);
+    if (use_mma) {
+        a.off_sinv = (int)sinv_off;
+    } else if (mma) {  // no tensor map for this buffer: the FFMA path
+        return fail(VB_EINVAL, "tensor-core ZNCC path needs 16-byte aligned uint16 frames");
+    }
 
     a.rows = split ? 16 : S;
     const int items = (pair ? 1 : fpi) * t.max_g * a.rows * nch;
@@ -1108,6 +1157,11 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
         a.n_frames = nb;
         a.partial = partial;
         a.inv = inv;
+        a.cov = inv;  // tensor-core path: the cross sums take the inv buffer's place
+        if (use_mma) {
+            rc = launch_zncc_mma(t, h, w, patch, radius, a.frames, nb, (int)f0, tmap_mma, inv, a.ss_pad, s);
+            if (rc) break;
+        }
         // persistent CTAs: each walks frames y, y+gy, ... (about 8 frames per CTA)
         const int64_t want_y = std::max<int64_t>(1, (int64_t)sms * 8 * 4 / std::max(1, t.n_groups));
         const unsigned gy = (unsigned)std::min<int64_t>(std::min<int64_t>(nb, 65535), std::max<int64_t>(want_y, (nb + 7) / 8));
@@ -1122,18 +1176,20 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
         launches().fetch_add(1, std::memory_order_relaxed);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) { rc = cuda_fail(e, "zncc_stats_kernel"); break; }
-        {
-            ZnccArgs as = a;
-            as.off_reg = (int)sp.off_reg;
-            as.off_z = (int)sp.off_z;
-            as.off_t = (int)sp.off_t;
-            as.off_inv = (inv_buf && a.use_tma) ? (int)((sp.total + 15) & ~(size_t)15) : -1;
-            ProfScope ps(kProfZncc, s);
-            fn<<<grid, threads, search_smem, s>>>(as, tmap);
+        if (!use_mma) {
+            {
+                ZnccArgs as = a;
+                as.off_reg = (int)sp.off_reg;
+                as.off_z = (int)sp.off_z;
+                as.off_t = (int)sp.off_t;
+                as.off_inv = (inv_buf && a.use_tma) ? (int)((sp.total + 15) & ~(size_t)15) : -1;
+                ProfScope ps(kProfZncc, s);
+                fn<<<grid, threads, search_smem, s>>>(as, tmap);
+            }
+            launches().fetch_add(1, std::memory_order_relaxed);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) { rc = cuda_fail(e, "zncc_group_kernel"); break; }
         }
-        launches().fetch_add(1, std::memory_order_relaxed);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) { rc = cuda_fail(e, "zncc_group_kernel"); break; }
         const int fin_blocks = (int)std::min<int64_t>(nb, 148 * 8);
         {
             ProfScope ps(kProfFinalize, s);

@@ -11,7 +11,9 @@ namespace vb {
 // Frames [T][H][W] of u16/f32 as a 3-D tensor {W, H, T} with a box of
 // {bw, bh, 1}.  Returns false (and the kernels fall back to plain loads) when
 // the layout violates TMA's 16-byte alignment rules.
-bool make_frames_tmap(CUtensorMap* map, const void* base, int dtype, int64_t t, int h, int w, int bh, int bw);
+// bt > 1: boxes of bt consecutive frames ({bw, bh, bt}).
+bool make_frames_tmap(CUtensorMap* map, const void* base, int dtype, int64_t t, int h, int w, int bh, int bw,
+                      int bt = 1);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
