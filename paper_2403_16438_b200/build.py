@@ -38,9 +38,14 @@ def build(force: bool = False, verbose: bool = False, experiments: bool = False)
     """experiments=True compiles the A/B switches (vb::knob) to read the
     environment (-DVB_EXPERIMENTS); the product build uses the defaults."""
     lib = LIB_EXP if experiments else LIB
+    extra = []
+    if experiments:  # A/B builds: extra compile-time variants, e.g. -DVB_PAIR_UNROLL=2 (build-time only)
+        extra = os.environ.get("VB_EXTRA_NVCC_FLAGS", "").split()
+        if os.environ.get("VB_EXP_NAME"):
+            lib = PKG / f"libvoltb200_{os.environ['VB_EXP_NAME']}.so"
     if not force and not _stale(lib):
         return lib
-    obj_dir = PKG / ("build_exp" if experiments else "build")
+    obj_dir = PKG / (("build_" + os.environ.get("VB_EXP_NAME", "exp")) if experiments else "build")
     obj_dir.mkdir(exist_ok=True)
     cc = nvcc()
     procs, objs = [], []
@@ -49,7 +54,7 @@ def build(force: bool = False, verbose: bool = False, experiments: bool = False)
         objs.append(obj)
         cmd = [cc, *ARCH, *FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
         if experiments:
-            cmd.append("-DVB_EXPERIMENTS")
+            cmd += ["-DVB_EXPERIMENTS", *extra]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         procs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
