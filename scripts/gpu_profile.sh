@@ -4,7 +4,7 @@
 set -u
 TAG=${1:-r01}
 OUT=gpurun_out
-CMD="python bench.py --frames 2000 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
+CMD="python bench.py --frames 2000 --steps 2 --warmup 1 --no-e2e --no-dropin --no-cpu-baseline"
 $CMD > $OUT/prof_plain_$TAG.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv $CMD > $OUT/ncu_launch_$TAG.log 2>&1
 echo "launch list rc=$?"
