@@ -114,8 +114,6 @@ struct vb_motion_plan {
 static void free_templates(Templates& t) {
     cudaFree(t.t16);
     cudaFree(t.tscale);
-    cudaFree(t.cen);
-    cudaFree(t.patch_group);
     cudaFree(t.tmpl);
     cudaFree(t.rvar);
     cudaFree(t.origins);
@@ -373,14 +371,8 @@ int vb_motion_plan_create(vb_motion_plan** out, int height, int width, int patch
     e = e ? e : cudaMemcpy(t.groups, groups.data(), groups.size() * sizeof(PatchGroup), cudaMemcpyHostToDevice);
     if (e == cudaSuccess && mma_supported(patch, radius, VB_U16)) {  // tensor-core path tables (uint16 frames)
         const MmaGeom g = mma_geom(patch, radius);
-        std::vector<int32_t> pg(n_origins);
-        for (size_t gi = 0; gi < groups.size(); ++gi)
-            for (int q = 0; q < groups[gi].count; ++q) pg[groups[gi].first + q] = (int32_t)gi;
-        e = e ? e : cudaMalloc(&t.t16, (size_t)n_origins * 8 * 2 * patch * g.tpw * 2);
-        e = e ? e : cudaMalloc(&t.tscale, (size_t)n_origins * sizeof(float));
-        e = e ? e : cudaMalloc(&t.cen, (size_t)n_origins * sizeof(int32_t));
-        e = e ? e : cudaMalloc(&t.patch_group, (size_t)n_origins * sizeof(int32_t));
-        e = e ? e : cudaMemcpy(t.patch_group, pg.data(), pg.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+        e = e ? e : cudaMalloc(&t.t16, (size_t)n_origins * 3 * 8 * patch * g.tpw);
+        e = e ? e : cudaMalloc(&t.tscale, (size_t)n_origins * sizeof(double));
     }
     if (e != cudaSuccess) {
         free_templates(t);

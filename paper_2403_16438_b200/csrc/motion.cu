@@ -137,8 +137,8 @@ struct ZnccArgs {
     int64_t n_frames;
     float* inv;       // [n_frames][N][S*S]  1/sqrt(fvar*rvar) (0 where the reference skips)
     double* partial;  // [n_frames][n_groups][S*S]
-    const float* cov; // COMBINE statistics: [n_frames][N][ss_pad] cross sums from zncc_mma_kernel
-    int off_sinv;     // COMBINE statistics: shared [G][ss_pad] inv rows
+    const float* cov;  // COMBINE statistics: [n_frames][N][ss_pad] window covariances (zncc_mma_kernel)
+    int off_sinv;      // COMBINE statistics: shared [G][ss_pad] inv rows
 };
 
 constexpr int kGenericDXB = 8;
@@ -237,10 +237,10 @@ __device__ __forceinline__ void store_row(float* out, const float (&v)[S]) {
     for (int i = head + 4 * nv; i < S; ++i) out[i] = v[i];
 }
 
-// COMBINE (tensor-core path): the inv rows stay in shared memory and the
-// kernel finishes the search -- partial[t][group][c] = sum over the group's
-// patches q (in order) of cov[t][q][c] * inv[q][c] in float64, the cross sums
-// coming from zncc_mma_kernel (no inv round trip through HBM).
+// COMBINE (tensor-core path, uint16): the kernel finishes the search -- the
+// inv rows stay in shared memory and partial[t][group][c] = sum over the
+// group's patches q (in order) of cov[t][q][c] * inv[q][c] in float64, the
+// covariances coming from zncc_mma_kernel (no inv round trip through HBM).
 template <bool INT, int P_CT, int S_CT = 0, bool COMBINE = false>
 __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __grid_constant__ CUtensorMap tmap) {
     using T1 = typename std::conditional<INT, int, double>::type;        // sample / sum of f
@@ -1115,7 +1115,7 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     // tensor-core path: boxes of one window row x 128 frames
     CUtensorMap tmap_mma;
     memset(&tmap_mma, 0, sizeof(tmap_mma));
-    const bool use_mma = mma && a.use_tma && make_frames_tmap(&tmap_mma, frames, dtype, n_frames, h, w, 1, 56, 128);
+    const bool use_mma = mma && a.use_tma && make_frames_tmap_sw128(&tmap_mma, frames, n_frames, h, w);
     if (use_mma) {
         a.off_sinv = (int)sinv_off;
     } else if (mma) {  // no tensor map for this buffer: the FFMA path
@@ -1132,6 +1132,7 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
 
     // frame batches bound the float64 partials + f32 inv buffers to ~1 GB
     const size_t per_frame_part = (size_t)t.n_groups * SS * sizeof(double);
+    // (the tensor-core path keeps the window covariances in this buffer instead of inv)
     const size_t per_frame_inv = (size_t)t.n * a.ss_pad * sizeof(float);
     int64_t batch = std::max<int64_t>(1, (int64_t)(((size_t)1 << 30) / (per_frame_part + per_frame_inv)));
     const int force_batch = knob("VB_ZNCC_BATCH", 0);  // experiment: frames per stats+search pair
@@ -1157,9 +1158,9 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
         a.n_frames = nb;
         a.partial = partial;
         a.inv = inv;
-        a.cov = inv;  // tensor-core path: the cross sums take the inv buffer's place
+        a.cov = inv;
         if (use_mma) {
-            rc = launch_zncc_mma(t, h, w, patch, radius, a.frames, nb, (int)f0, tmap_mma, inv, a.ss_pad, s);
+            rc = launch_zncc_mma(t, patch, radius, nb, (int)f0, tmap_mma, inv, a.ss_pad, s);
             if (rc) break;
         }
         // persistent CTAs: each walks frames y, y+gy, ... (about 8 frames per CTA)

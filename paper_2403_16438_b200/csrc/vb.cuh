@@ -97,24 +97,24 @@ struct Templates {
     PatchGroup* groups = nullptr;// [n_groups]
     int n = 0, n_groups = 0, tp = 0, max_g = 0, max_wu = 0;
     int pitch = 0;               // f32 region row pitch of the search kernel (bank-conflict tuned)
-    // tensor-core path (zncc_mma.cu; uint16 frames): f16 split template rows
-    // [N][8 shifts][2 parts][P][tpw], per-patch scale 2^-e and centre, patch -> group
+    // tensor-core path (zncc_mma.cu; uint16 frames): signed digit planes of
+    // the fixed-point template [N][3][8 shifts][P][tpw] (int8), per-patch 2^-s
     void* t16 = nullptr;
-    float* tscale = nullptr;
-    int32_t* cen = nullptr;
-    int32_t* patch_group = nullptr;
+    double* tscale = nullptr;
 };
 
 // Geometry of the tensor-core ZNCC path for (patch, radius) (zncc_mma.cu).
 struct MmaGeom {
-    int wx = 0, wxp = 0, toff = 0, tpw = 0, np = 0, npass = 0, nchunks = 0;
-    size_t off_a = 0, off_b = 0, smem = 0;
+    int wx = 0, wxp = 0, toff = 0, tpw = 0, npass = 0, nchunks = 0, na = 0, nb = 0;
+    int np[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    size_t off_a = 0, off_b = 0, b_bytes = 0, off_tq = 0, smem = 0;
 };
 bool mma_supported(int patch, int radius, int dtype);
 MmaGeom mma_geom(int patch, int radius);
+bool make_frames_tmap_sw128(CUtensorMap* map, const void* base, int64_t t, int h, int w);
 int launch_mma_prep(const Templates& t, int patch, int radius, cudaStream_t s);
-int launch_zncc_mma(const Templates& t, int h, int w, int patch, int radius, const void* frames, int64_t n_frames,
-                    int tma_z0, const CUtensorMap& tmap, float* cov, int ss_pad, cudaStream_t s);
+int launch_zncc_mma(const Templates& t, int patch, int radius, int64_t n_frames, int tma_z0, const CUtensorMap& tmap,
+                    float* cov, int ss_pad, cudaStream_t s);
 
 // Kernel entry points implemented in the .cu files (host-side launchers).
 int launch_template_sum(const void* frames, int dtype, int64_t n, int64_t hw, double* sum,
