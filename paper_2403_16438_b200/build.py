@@ -13,7 +13,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libvoltb200.so"
 LIB_EXP = PKG / "libvoltb200_exp.so"  # experiment build (A/B switches live); loaded only via VB_LIBRARY
-SOURCES = ["capi.cu", "stage.cu", "group.cu", "motion.cu", "zncc_mma.cu", "summary.cu", "probe.cu", "traces.cu", "unet.cu"]
+SOURCES = ["capi.cu", "stage.cu", "group.cu", "motion.cu", "summary.cu", "probe.cu", "traces.cu", "unet.cu"]
+EXP_SOURCES = ["zncc_mma.cu"]  # measured no-go prototypes, experiment build only
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-O3",
          f"-I{ROOT / 'include'}"]
@@ -30,7 +31,7 @@ def _stale(lib: Path = LIB) -> bool:
     if not lib.exists():
         return True
     t = lib.stat().st_mtime
-    deps = [CSRC / s for s in SOURCES] + [CSRC / "vb.cuh", CSRC / "tma.cuh", ROOT / "include" / "voltb200.h"]
+    deps = [CSRC / s for s in SOURCES + EXP_SOURCES] + [CSRC / "vb.cuh", CSRC / "tma.cuh", ROOT / "include" / "voltb200.h"]
     return any(d.stat().st_mtime > t for d in deps)
 
 
@@ -49,7 +50,7 @@ def build(force: bool = False, verbose: bool = False, experiments: bool = False)
     obj_dir.mkdir(exist_ok=True)
     cc = nvcc()
     procs, objs = [], []
-    for src in SOURCES:
+    for src in SOURCES + (EXP_SOURCES if experiments else []):
         obj = obj_dir / (Path(src).stem + ".o")
         objs.append(obj)
         cmd = [cc, *ARCH, *FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
@@ -59,7 +60,7 @@ def build(force: bool = False, verbose: bool = False, experiments: bool = False)
             cmd += ["-Xptxas", "-v"]
         procs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
     failed = []
-    for src, p in zip(SOURCES, procs):
+    for src, p in zip(SOURCES + (EXP_SOURCES if experiments else []), procs):
         out, _ = p.communicate()
         if verbose or p.returncode:
             sys.stderr.write(out)

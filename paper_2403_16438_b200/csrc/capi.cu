@@ -369,11 +369,13 @@ int vb_motion_plan_create(vb_motion_plan** out, int height, int width, int patch
     e = e ? e : cudaMemcpy(t.origins, origins_host, (size_t)n_origins * 2 * sizeof(int32_t), cudaMemcpyHostToDevice);
     e = e ? e : cudaMemcpy(t.patch_col, col.data(), col.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
     e = e ? e : cudaMemcpy(t.groups, groups.data(), groups.size() * sizeof(PatchGroup), cudaMemcpyHostToDevice);
+#ifdef VB_EXPERIMENTS
     if (e == cudaSuccess && mma_supported(patch, radius, VB_U16)) {  // tensor-core path tables (uint16 frames)
         const MmaGeom g = mma_geom(patch, radius);
         e = e ? e : cudaMalloc(&t.t16, (size_t)n_origins * 3 * 8 * patch * g.tpw);
         e = e ? e : cudaMalloc(&t.tscale, (size_t)n_origins * sizeof(double));
     }
+#endif
     if (e != cudaSuccess) {
         free_templates(t);
         delete p;
@@ -386,7 +388,9 @@ int vb_motion_plan_create(vb_motion_plan** out, int height, int width, int patch
 int vb_motion_plan_set_reference(vb_motion_plan* p, const float* ref_dev, void* stream) {
     if (!p || !ref_dev) return fail(VB_EINVAL, "null argument");
     int rc = launch_prep_templates(ref_dev, p->h, p->w, p->patch, p->t, (cudaStream_t)stream);
+#ifdef VB_EXPERIMENTS
     if (rc == VB_OK && p->t.t16) rc = launch_mma_prep(p->t, p->patch, p->radius, (cudaStream_t)stream);
+#endif
     if (rc == VB_OK) p->have_ref = true;
     return rc;
 }

@@ -1052,7 +1052,8 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
         if (S == 25) stats_fn = zncc_stats_kernel<true, 21, 25>;
         if (S == 11) stats_fn = zncc_stats_kernel<true, 21, 11>;
     }
-    // tensor-core cross sums (zncc_mma.cu) + combining statistics kernel, uint16 frames
+    // tensor-core cross sums (zncc_mma.cu, experiment build) + combining statistics kernel
+#ifdef VB_EXPERIMENTS
     const bool mma = dtype == VB_U16 && t.t16 != nullptr && mma_supported(patch, radius, dtype);
     if (mma) {
         stats_fn = zncc_stats_kernel<true, 0, 0, true>;
@@ -1065,6 +1066,9 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
             stats_fn = zncc_stats_kernel<true, 21, 0, true>;
         }
     }
+#else
+    const bool mma = false;
+#endif
     SmemPlan sp = zncc_smem(patch, radius, t.max_g, t.max_wu, dtype, fpi, fast, t.pitch);
     const int ss_pad_c = (S * S + 3) & ~3;
     const size_t sinv_off = (sp.stats_total + 15) & ~(size_t)15;
@@ -1115,7 +1119,11 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
     // tensor-core path: boxes of one window row x 128 frames
     CUtensorMap tmap_mma;
     memset(&tmap_mma, 0, sizeof(tmap_mma));
+#ifdef VB_EXPERIMENTS
     const bool use_mma = mma && a.use_tma && make_frames_tmap_sw128(&tmap_mma, frames, n_frames, h, w);
+#else
+    const bool use_mma = false;
+#endif
     if (use_mma) {
         a.off_sinv = (int)sinv_off;
     } else if (mma) {  // no tensor map for this buffer: the FFMA path
@@ -1159,10 +1167,12 @@ int launch_motion(const Templates& t, int h, int w, int patch, int radius, const
         a.partial = partial;
         a.inv = inv;
         a.cov = inv;
+#ifdef VB_EXPERIMENTS
         if (use_mma) {
             rc = launch_zncc_mma(t, patch, radius, nb, (int)f0, tmap_mma, inv, a.ss_pad, s);
             if (rc) break;
         }
+#endif
         // persistent CTAs: each walks frames y, y+gy, ... (about 8 frames per CTA)
         const int64_t want_y = std::max<int64_t>(1, (int64_t)sms * 8 * 4 / std::max(1, t.n_groups));
         const unsigned gy = (unsigned)std::min<int64_t>(std::min<int64_t>(nb, 65535), std::max<int64_t>(want_y, (nb + 7) / 8));
