@@ -235,7 +235,8 @@ class _PinnedBlock:
 
     def __init__(self, pool: "PinnedPool", ptr: int, nbytes: int, shape: tuple, dtype: np.dtype):
         self.__array_interface__ = {"data": (ptr, False), "shape": shape, "typestr": dtype.str, "version": 3}
-        weakref.finalize(self, pool._release, ptr, nbytes)
+        fin = weakref.finalize(self, pool._release, ptr, nbytes)
+        fin.atexit = False  # at interpreter exit the process releases page-locked memory itself
 
 
 class PinnedPool:
