@@ -363,3 +363,18 @@ def test_device_group_equals_single_device(cuda, c1_small):
     np.testing.assert_array_equal(sp, s2)
     np.testing.assert_array_equal(tp, t2)
     np.testing.assert_array_equal(corr, c2)
+
+
+def test_device_group_errors(cuda, c1_small):
+    """vb_group argument checks (reference error texts where they exist)."""
+    from paper_2403_16438_b200.stage import GroupStage
+
+    cfg, raw = c1_small
+    with pytest.raises(ValueError, match="distinct"):
+        GroupStage(raw.shape[1], raw.shape[2], _stage_cfg(cfg, 100), devices=[0, 0])
+    g = GroupStage(raw.shape[1], raw.shape[2], _stage_cfg(cfg, 100), devices=[0])
+    try:
+        with pytest.raises(ValueError, match="at least 2 frames"):
+            g.run(raw[:101])
+    finally:
+        g.close()
