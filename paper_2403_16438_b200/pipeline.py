@@ -12,6 +12,7 @@ no host threads.  Stage timings mirror _StageTimer (pipeline.py:133-142).
 """
 from __future__ import annotations
 
+import json
 import time
 from dataclasses import dataclass, field
 
@@ -24,6 +25,37 @@ from .summarize import SummaryPair
 from .video import Video
 
 
+MIN_STAGE_SECONDS = 1e-3  # evaluate.py:16
+
+
+@dataclass
+class ThroughputReport:
+    """evaluate.py:83-101: per-stage wall seconds, the run's total, frames/s
+    and the ratio to the recording's real-time frame rate."""
+    stage_seconds: dict
+    total_seconds: float
+    frames: int
+    effective_fps: float
+    target_fps: float | None = None
+    realtime_ratio: float | None = None
+
+    def to_json(self) -> str:
+        keys = ("stage_seconds", "total_seconds", "frames", "effective_fps", "target_fps", "realtime_ratio")
+        return json.dumps({k: getattr(self, k) for k in keys}, indent=2)
+
+
+def throughput_report(frames: int, stage_seconds: dict, target_fps: float | None = None,
+                      total_seconds: float | None = None) -> ThroughputReport:
+    """evaluate.py:103-125.  The total defaults to the sum of the stages (pass
+    it explicitly when stages overlap); totals under 1 ms clamp to 1 ms."""
+    total = sum(stage_seconds.values()) if total_seconds is None else total_seconds
+    total = max(total, MIN_STAGE_SECONDS)
+    fps = frames / total
+    return ThroughputReport(stage_seconds=dict(stage_seconds), total_seconds=total, frames=frames,
+                            effective_fps=fps, target_fps=target_fps,
+                            realtime_ratio=fps / target_fps if target_fps else None)
+
+
 @dataclass
 class SegmentationResult:
     """The fields of the reference's PipelineResult this path produces."""
@@ -32,6 +64,7 @@ class SegmentationResult:
     probability_maps: list = field(default_factory=list)     # list[ProbabilityMap]
     corrected: Video | None = None
     seconds: dict = field(default_factory=dict)              # {"motion+segment": wall seconds}
+    throughput: ThroughputReport | None = None               # pipeline.py:171-172
 
 
 def run_motion_and_segment(video, weights: U.WeightBundle, *, patch_size: int = M.DEFAULT_PATCH_SIZE,
@@ -57,5 +90,6 @@ def run_motion_and_segment(video, weights: U.WeightBundle, *, patch_size: int = 
     res.pairs = [SummaryPair(i, sp[i], tp[i]) for i in range(sp.shape[0])]
     res.probability_maps = [U.ProbabilityMap(i, prob[i]) for i in range(prob.shape[0])]
     res.corrected = Video(corr, frame_rate=v.frame_rate) if corr is not None else None
-    res.seconds = {"motion+segment": dt}
+    res.seconds = {"motion+segment": dt}  # one overlapped device pass: the stages share their wall time
+    res.throughput = throughput_report(v.frames, res.seconds, v.frame_rate, total_seconds=dt)
     return res

@@ -32,6 +32,9 @@ def test_motion_and_segment_matches_reference_pipeline(cuda, golden):
         assert pm.segment_index == i
         np.testing.assert_allclose(res.pairs[i].spatial, golden["spatial"][i], rtol=1e-4, atol=1e-3)
         assert np.abs(pm.values - golden["prob"][i]).max() <= 1e-4
+    rep = res.throughput  # pipeline.py:171-172
+    assert rep.frames == golden["raw"].shape[0] and rep.total_seconds >= 1e-3
+    assert rep.effective_fps == pytest.approx(rep.frames / rep.total_seconds)
 
 
 @pytest.mark.parametrize("chunk", [60, 120, 0])
