@@ -65,6 +65,29 @@ class TestGaussian:  # test_summarize.py:75-95
                                          3.0, axis=1, mode="reflect", radius=9)
         np.testing.assert_array_equal(gaussian_smooth(x, 3.0), want)
 
+    @pytest.mark.parametrize("kind", ["mixed_scales", "zeros_and_spikes", "signed", "tiny"])
+    @pytest.mark.parametrize("shape", [(64, 128), (70, 130)])
+    def test_bit_exact_adversarial(self, cuda, rng, kind, shape):
+        """Inputs that put outputs near float32 rounding midpoints relative to
+        the tile's largest sample (the R = 9 kernels' fused float64 passes
+        must then fall back to scipy's unfused order): mixed magnitudes,
+        zero fields with isolated spikes, signed values, subnormal-range data."""
+        if kind == "mixed_scales":
+            x = rng.standard_normal(shape) * 10.0 ** rng.integers(-6, 7, shape)
+        elif kind == "zeros_and_spikes":
+            x = np.zeros(shape)
+            idx = rng.integers(0, x.size, x.size // 50)
+            x.flat[idx] = rng.random(idx.size) * 6e4
+            x[::7] += 1e-3
+        elif kind == "signed":
+            x = rng.standard_normal(shape) * 1000.0
+        else:
+            x = rng.standard_normal(shape) * 1e-36
+        x = x.astype(np.float32)
+        want = ndimage.gaussian_filter1d(ndimage.gaussian_filter1d(x, 3.0, axis=0, mode="reflect", radius=9),
+                                         3.0, axis=1, mode="reflect", radius=9)
+        np.testing.assert_array_equal(gaussian_smooth(x, 3.0), want)
+
     def test_golden_impulse(self, cuda, golden):
         z = golden("summary")
         np.testing.assert_array_equal(gaussian_smooth(z["gauss_impulse"], 3.0), z["gauss_impulse_out"])
