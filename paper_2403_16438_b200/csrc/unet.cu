@@ -64,6 +64,7 @@ struct ConvArgs {
     const float* w1;     // final 1x1 kernel [cout] (cout -> 1) or null
     const float* b1;     // final 1x1 bias [1]
     float* prob;         // [n][h][w] sigmoid(1x1) or null
+    int dbg;             // experiment build: 1 skip the MMAs, 2 skip the activation/weight staging
 };
 
 // Register-blocked tile geometry per output width: every thread owns a
@@ -424,22 +425,34 @@ __global__ void __launch_bounds__(128) conv3x3_tc_kernel(ConvArgs a) {
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
             smem_u32(&bar[0])));
     };
+#ifdef VB_EXPERIMENTS
+    const int dbg = a.dbg;  // time the staging and the MMAs separately (scripts/ab_unet_dbg.sh)
+#else
+    constexpr int dbg = 0;
+#endif
     uint32_t ph = 0;
-    load_rows(0);
+    if (dbg != 2) load_rows(0);
     for (int ch = 0; ch < nchunks; ++ch) {
         if (ch > 0) {  // the previous chunk's MMAs have read the K-major planes and weights
             mbar_wait(&bar[0], ph);
             ph ^= 1u;
         }
-        fetch_w(ch);
-        store_rows();
+        if (dbg != 2) {
+            fetch_w(ch);
+            store_rows();
+        }
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;\n");
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;\n");
-        if (tid == 0) issue(ch);
-        if (ch + 1 < nchunks) load_rows(ch + 1);  // in flight during this chunk's MMAs
+        if (tid == 0) {
+            if (dbg != 1)
+                issue(ch);
+            else
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&bar[0])) : "memory");
+        }
+        if (ch + 1 < nchunks && dbg != 2) load_rows(ch + 1);  // in flight during this chunk's MMAs
     }
     mbar_wait(&bar[0], ph);
     asm volatile("tcgen05.fence::after_thread_sync;\n");
@@ -509,7 +522,9 @@ int launch_conv_tc(const ConvArgs& a, cudaStream_t s) {
     return VB_OK;
 }
 
-int conv(const ConvArgs& a, cudaStream_t s) {
+int conv(const ConvArgs& a0, cudaStream_t s) {
+    ConvArgs a = a0;
+    a.dbg = knob("VB_UNET_DBG", 0);
     if (!knob("VB_UNET_SIMT", 0)) {  // experiment: FP32 SIMT kernels
         if (a.cout <= 16) return launch_conv_tc<16>(a, s);
         if (a.cout <= 32) return launch_conv_tc<32>(a, s);
