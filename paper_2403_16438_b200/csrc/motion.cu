@@ -409,6 +409,9 @@ __global__ void __launch_bounds__(256) zncc_stats_kernel(ZnccArgs a, const __gri
 // Cross sums for one (patch, dy) row of S candidates, compile-time P and S.
 // Template taps come from the prepared patch in global memory (L1-resident,
 // warp-broadcast): every lane of a patch reads the same float4.
+#ifndef VB_PAIR_IL
+#define VB_PAIR_IL 1  // paired split kernel: the two frames' regions interleaved, one 64-bit load per window sample (measured: C2 search 5.84 -> 5.74 ms per 4000 frames; 0 = separate regions)
+#endif
 #ifndef VB_GEN_UNROLL
 #define VB_GEN_UNROLL 1  // measured: 2 -> C3 search 13.54 -> 16.75 ms (115 registers)
 #endif
@@ -507,8 +510,19 @@ __device__ __forceinline__ void lane_shfl_add(float2& v, int off) {
     v.y += __shfl_down_sync(0xffffffffu, v.y, off, 16);
 }
 
-// fstride: floats between the two frames' regions (V = float2)
-template <int P, typename V, int PF = VB_SPLIT_PREFETCH>
+// Interleaved pair regions (CS = 2): the two frames' samples of one region
+// position are adjacent, one 64-bit shared load per window sample.
+template <int CS, typename V>
+__device__ __forceinline__ void lane_load_cs(V& v, const float* p, int fstride) {
+    if constexpr (CS == 2)
+        v = *reinterpret_cast<const float2*>(p);
+    else
+        lane_load(v, p, fstride);
+}
+
+// fstride: floats between the two frames' regions (V = float2, CS = 1);
+// CS: floats per region column (2 = interleaved pair, pitch in floats)
+template <int P, typename V, int PF = VB_SPLIT_PREFETCH, int CS = 1>
 __device__ __forceinline__ void cross_row_split17(const float* __restrict__ reg, int pitch, int fstride,
                                                   const float* __restrict__ trow0, int tp, int d, V (&acc)[17],
                                                   V (&accm)[17]) {
@@ -528,7 +542,7 @@ __device__ __forceinline__ void cross_row_split17(const float* __restrict__ reg,
     for (int q = 0; q < TQ; ++q) t_next[q] = __ldg(reinterpret_cast<const float4*>(trow0) + q);
     V w_next[PF];
 #pragma unroll
-    for (int i = 0; i < PF; ++i) lane_load(w_next[i], reg + i, fstride);
+    for (int i = 0; i < PF; ++i) lane_load_cs<CS>(w_next[i], reg + CS * i, fstride);
 #endif
     constexpr int kUnroll = std::is_same<V, float2>::value ? kSplitUnrollPair : kSplitUnroll;
 #pragma unroll kUnroll
@@ -540,7 +554,7 @@ __device__ __forceinline__ void cross_row_split17(const float* __restrict__ reg,
 #pragma unroll
         for (int i = 0; i < PF; ++i) win[i] = w_next[i];
 #pragma unroll
-        for (int i = PF; i < S + P - 1; ++i) lane_load(win[i], fr + i, fstride);
+        for (int i = PF; i < S + P - 1; ++i) lane_load_cs<CS>(win[i], fr + CS * i, fstride);
 #pragma unroll
         for (int q = 0; q < TQ; ++q) {
             tv[4 * q] = t_next[q].x;
@@ -562,11 +576,11 @@ __device__ __forceinline__ void cross_row_split17(const float* __restrict__ reg,
 #pragma unroll
             for (int q = 0; q < TQ; ++q) t_next[q] = __ldg(reinterpret_cast<const float4*>(trow0 + yn * tp) + q);
 #pragma unroll
-            for (int i = 0; i < PF; ++i) lane_load(w_next[i], reg + yn * pitch + i, fstride);
+            for (int i = 0; i < PF; ++i) lane_load_cs<CS>(w_next[i], reg + yn * pitch + CS * i, fstride);
         }
 #else
 #pragma unroll
-        for (int i = 0; i < S + P - 1; ++i) lane_load(win[i], fr + i, fstride);
+        for (int i = 0; i < S + P - 1; ++i) lane_load_cs<CS>(win[i], fr + CS * i, fstride);
         {
             const float4* trow = reinterpret_cast<const float4*>(trow0 + yy * tp);
 #pragma unroll
@@ -637,6 +651,13 @@ __global__ void __launch_bounds__(SPLIT ? 128 : 288, SPLIT ? (FPI == 2 ? 2 : kSp
     const int tid = threadIdx.x, nth = blockDim.x;
     const float cg = group_centre(a, grp);
     const float magic = 8388608.0f + cg;
+    constexpr bool kIL = SPLIT && FPI == 2 && VB_PAIR_IL;  // interleaved pair regions
+    constexpr int CS = kIL ? 2 : 1;
+    // region of frame f, padded row r, column c (floats)
+    auto reg_at = [&](int f, int r, int c) -> float* {
+        return kIL ? reinterpret_cast<float*>(smem + a.off_reg) + 2 * (r * pitch + c) + f
+                   : reinterpret_cast<float*>(smem + a.off_reg + f * reg_slot) + r * pitch + c;
+    };
     const int boff = box_off(a, grp);
     if (tid == 0 && a.use_tma) {
 #pragma unroll
@@ -673,7 +694,7 @@ __global__ void __launch_bounds__(SPLIT ? 128 : 288, SPLIT ? (FPI == 2 ? 2 : kSp
             for (int u = tid; u < nf * wu; u += nth) {
                 const int f = u >= wu ? 1 : 0, c = u - f * wu;
                 const uint16_t* raw = reinterpret_cast<const uint16_t*>(smem + f * raw_slot) + boff + c;
-                float* reg = reinterpret_cast<float*>(smem + a.off_reg + f * reg_slot) + c;
+                float* reg = reg_at(f, 0, c);
 #pragma unroll
                 for (int r0 = 0; r0 < RHC; r0 += 16) {
                     uint32_t v[16];
@@ -682,14 +703,14 @@ __global__ void __launch_bounds__(SPLIT ? 128 : 288, SPLIT ? (FPI == 2 ? 2 : kSp
                         if (r0 + k < RHC) v[k] = raw[(r0 + k) * a.bw];
 #pragma unroll
                     for (int k = 0; k < 16; ++k)
-                        if (r0 + k < RHC) reg[(r0 + k) * pitch] = u16_minus(v[k], magic);
+                        if (r0 + k < RHC) reg[(r0 + k) * pitch * CS] = u16_minus(v[k], magic);
                 }
             }
         } else {
             const int lane = tid & 31, nw = nth >> 5;
             for (int fr = tid >> 5; fr < nf * RH; fr += nw) {
                 const int f = fr / RH, r = fr - f * RH;
-                float* reg = reinterpret_cast<float*>(smem + a.off_reg + f * reg_slot) + r * pitch;
+                float* reg = reg_at(f, r, 0);
                 if (SPLIT && a.dtype == VB_U16 && wu <= 256 && a.conv_batch) {  // loads first, then converts (LDS latency overlapped)
                     const uint16_t* raw = reinterpret_cast<const uint16_t*>(smem + f * raw_slot) + boff + r * a.bw;
                     uint32_t v[8];
@@ -697,13 +718,13 @@ __global__ void __launch_bounds__(SPLIT ? 128 : 288, SPLIT ? (FPI == 2 ? 2 : kSp
                     for (int k = 0; k < 8; ++k) v[k] = lane + 32 * k < wu ? raw[lane + 32 * k] : 0u;
 #pragma unroll
                     for (int k = 0; k < 8; ++k)
-                        if (lane + 32 * k < wu) reg[lane + 32 * k] = u16_minus(v[k], magic);
+                        if (lane + 32 * k < wu) reg[CS * (lane + 32 * k)] = u16_minus(v[k], magic);
                 } else if (a.dtype == VB_U16) {
                     const uint16_t* raw = reinterpret_cast<const uint16_t*>(smem + f * raw_slot) + boff + r * a.bw;
-                    for (int c = lane; c < wu; c += 32) reg[c] = u16_minus(raw[c], magic);
+                    for (int c = lane; c < wu; c += 32) reg[CS * c] = u16_minus(raw[c], magic);
                 } else {
                     const float* raw = reinterpret_cast<const float*>(smem + f * raw_slot) + boff + r * a.bw;
-                    for (int c = lane; c < wu; c += 32) reg[c] = __fsub_rn(raw[c], cg);
+                    for (int c = lane; c < wu; c += 32) reg[CS * c] = __fsub_rn(raw[c], cg);
                 }
             }
         }
@@ -740,9 +761,10 @@ __global__ void __launch_bounds__(SPLIT ? 128 : 288, SPLIT ? (FPI == 2 ? 2 : kSp
             float2 acc[17], accm[17];
             if (valid) {
                 const int col = a.patch_col[grp.first + p];
-                const float* reg = reinterpret_cast<const float*>(smem + a.off_reg) + d * pitch + col;
-                cross_row_split17<21, float2, VB_SPLIT_PREFETCH_PAIR>(reg, pitch, (int)(reg_slot / 4), a.tmpl + (size_t)(grp.first + p) * P * tp, tp, d,
-                                      acc, accm);
+                const float* reg = reg_at(0, d, col);
+                cross_row_split17<21, float2, VB_SPLIT_PREFETCH_PAIR, CS>(reg, pitch * CS, (int)(reg_slot / 4),
+                                                                          a.tmpl + (size_t)(grp.first + p) * P * tp, tp,
+                                                                          d, acc, accm);
             } else {
 #pragma unroll
                 for (int i = 0; i < 17; ++i) acc[i] = accm[i] = make_float2(0.0f, 0.0f);
