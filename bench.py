@@ -392,13 +392,14 @@ def run_ours(args):
             traffic_src = z["source"] + "; scaled to this run's frames per launch"
         except (ValueError, KeyError):
             pass
-    # bytes the search kernel moves by design per launch: the u16 frames (TMA
-    # boxes, union windows overlap only inside a group), the statistics
-    # kernel's 1/sqrt(var) per (patch, candidate) and the float64 group partials
+    # the search kernel's algorithmic bytes are its input, the u16 frame; the
+    # statistics kernel's 1/sqrt(var) per (patch, candidate) (read) and the
+    # float64 group partials (written) are this design's intermediates and are
+    # reported separately, so traffic / traffic_algorithmic shows their cost
     info = pre.plan.info()
     sdim = 2 * cfg.radius + 1
-    search_bytes_frame = (cfg.height * cfg.width * 2 + 4 * info["patches"] * sdim * sdim
-                          + 8 * info["groups"] * sdim * sdim)
+    frame_bytes = cfg.height * cfg.width * 2
+    inter_bytes_frame = 4 * info["patches"] * sdim * sdim + 8 * info["groups"] * sdim * sdim
     kernel_ms_per_step = {n: float(ms[i] / args.steps) for i, n in
                           enumerate(["zncc_group", "finalize", "warp_smooth", "median", "other"])}
     hbm_stage = bytes_frame * total_frames / world / (step_ms / 1e3) / 1e9
@@ -413,9 +414,11 @@ def run_ours(args):
         "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
         "traffic": traffic,
         "traffic_source": traffic_src,
-        "traffic_algorithmic": search_bytes_frame * frames_per_launch,
-        "traffic_algorithmic_def": "per launch: frames x (2*H*W u16 frame + 4*N*S^2 inv from the statistics kernel "
-                                   "+ 8*groups*S^2 float64 partials)",
+        "traffic_algorithmic": frame_bytes * frames_per_launch,
+        "traffic_algorithmic_def": "per launch: frames x 2*H*W (the u16 frames the search reads)",
+        "traffic_intermediates": inter_bytes_frame * frames_per_launch,
+        "traffic_intermediates_def": "per launch: frames x (4*N*S^2 inv rows from the statistics kernel + "
+                                     "8*groups*S^2 float64 group partials to the finalize kernel)",
         "peak_source": "measured live: FFMA2 (fma.rn.f32x2) probe, vb_fp32_peak_probe",
         "peak_ffma_scalar": p1.value,
         "algorithmic": f"{flops_frame:.4g} flop/frame = 2*N_patch({n_patches})*(2r+1)^2*21^2; "
