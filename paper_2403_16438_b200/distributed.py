@@ -313,11 +313,21 @@ class DeviceOps:
         self.pre.plan.set_reference(ref)
         self.pre.set_shading(ref)
 
-    def estimate(self, frames):
+    def estimate(self, frames, arrival=None, chunk=0):
+        """Motion vectors of every frame; with `arrival` the search runs in
+        chunks of `chunk` frames, each after arrival(a, b) has made the stream
+        wait for frames [a, b) (uploads still streaming in)."""
         from . import _device as D
 
-        vec = D.empty_motion(frames.shape[0], frames.device)
-        self.pre.plan.estimate(frames, self.cfg.subpixel, out=vec)
+        n = frames.shape[0]
+        vec = D.empty_motion(n, frames.device)
+        if arrival is None or chunk <= 0:
+            self.pre.plan.estimate(frames, self.cfg.subpixel, out=vec)
+            return vec
+        for a in range(0, n, chunk):
+            b = min(n, a + chunk)
+            arrival(a, b)
+            self.pre.plan.estimate(frames[a:b], self.cfg.subpixel, out=self.vec_slice(vec, a, b))
         return vec
 
     @staticmethod
@@ -505,16 +515,30 @@ class BalancedShardedPreprocessor:
         self._runs = 0
         self._tail_next = None
 
-    def run(self, frames_local, shard: BalancedShard, ref_frames: int, corrected_out=None) -> ShardResult:
+    def run(self, frames_local, shard: BalancedShard, ref_frames: int, corrected_out=None,
+            arrival=None, chunk: int = 0) -> ShardResult:
         """frames_local = recording frames [shard.local_lo, shard.local_hi);
-        corrected_out (optional) = [shard.frames, H, W] for the shard's own frames."""
+        corrected_out (optional) = [shard.frames, H, W] for the shard's own frames.
+        arrival (optional, streamed uploads): arrival(a, b) makes the current
+        stream wait until local frames [a, b) are resident; the template waits
+        for its rows, the motion search runs in chunks of `chunk` frames as they
+        land, and the summaries start once every frame is in."""
         ops, s = self.ops, shard
         base, T, f0 = s.local_lo, s.n_total, s.frame_lo
-        if frames_local.shape[0] != s.local_hi - s.local_lo:
+        n_local = s.local_hi - s.local_lo
+        if frames_local.shape[0] != n_local:
             raise ValueError("frames_local must hold the shard and its halo")
         lo, hi = template_rows(Shard(s.rank, s.world, s.frame_lo, s.frame_hi, 0, 0, T), ref_frames, base)
+        if arrival is not None and hi > lo:
+            arrival(lo, hi)
         ops.template(frames_local, lo, hi, min(ref_frames, T), self.group)
-        vec = ops.estimate(frames_local)
+        if arrival is not None and chunk > 0:
+            vec = ops.estimate(frames_local, arrival, chunk)
+            arrival(0, n_local)
+        else:
+            if arrival is not None:
+                arrival(0, n_local)
+            vec = ops.estimate(frames_local)
 
         def corr(a, b):
             return None if corrected_out is None else corrected_out[a - f0:b - f0]
