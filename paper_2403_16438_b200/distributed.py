@@ -313,10 +313,11 @@ class DeviceOps:
         self.pre.plan.set_reference(ref)
         self.pre.set_shading(ref)
 
-    def estimate(self, frames, arrival=None, chunk=0):
+    def estimate(self, frames, arrival=None, chunk=0, after=None):
         """Motion vectors of every frame; with `arrival` the search runs in
         chunks of `chunk` frames, each after arrival(a, b) has made the stream
-        wait for frames [a, b) (uploads still streaming in)."""
+        wait for frames [a, b) (uploads still streaming in), and after(vec, b)
+        is called once frames [0, b) are searched."""
         from . import _device as D
 
         n = frames.shape[0]
@@ -328,6 +329,8 @@ class DeviceOps:
             b = min(n, a + chunk)
             arrival(a, b)
             self.pre.plan.estimate(frames[a:b], self.cfg.subpixel, out=self.vec_slice(vec, a, b))
+            if after is not None:
+                after(vec, b)
         return vec
 
     @staticmethod
@@ -514,6 +517,7 @@ class BalancedShardedPreprocessor:
         self._tokens = None
         self._runs = 0
         self._tail_next = None
+        self._whole = None
 
     def run(self, frames_local, shard: BalancedShard, ref_frames: int, corrected_out=None,
             arrival=None, chunk: int = 0) -> ShardResult:
@@ -532,16 +536,32 @@ class BalancedShardedPreprocessor:
         if arrival is not None and hi > lo:
             arrival(lo, hi)
         ops.template(frames_local, lo, hi, min(ref_frames, T), self.group)
+
+        def corr(a, b):
+            return None if corrected_out is None else corrected_out[a - f0:b - f0]
+
+        self._whole = None
         if arrival is not None and chunk > 0:
-            vec = ops.estimate(frames_local, arrival, chunk)
+            # whole blocks are summarised as soon as their frames are searched,
+            # while later pieces are still uploading
+            wl, wh, L = s.whole_lo - base, s.whole_hi - base, ops.cfg.segment_length
+            parts, done = [], [wl]
+
+            def after(vec, b):
+                while done[0] < wh and min(done[0] + L, wh) <= b:
+                    e = min(done[0] + L, wh)
+                    parts.append(ops.whole(frames_local, vec, base, T, (done[0], e - done[0]),
+                                           corr(done[0] + base, e + base)))
+                    done[0] = e
+
+            vec = ops.estimate(frames_local, arrival, chunk, after)
             arrival(0, n_local)
+            if parts:
+                self._whole = (torch.cat([p[0] for p in parts]), torch.cat([p[1] for p in parts]))
         else:
             if arrival is not None:
                 arrival(0, n_local)
             vec = ops.estimate(frames_local)
-
-        def corr(a, b):
-            return None if corrected_out is None else corrected_out[a - f0:b - f0]
 
         def run_piece(p: Piece, smoothed, acc):
             ops.piece(frames_local[p.c_lo - base:p.c_hi - base], ops.vec_slice(vec, p.c_lo - base, p.c_hi - base),
@@ -564,8 +584,8 @@ class BalancedShardedPreprocessor:
             recvs.append(([head_buf[:p.c_lo - p.s_lo], head_sum], p.prev))
         handle = p2p.start(sends, recvs) if (sends or recvs) else None
         sp_parts, tp_parts = [], []
-        whole = None
-        if s.whole_hi > s.whole_lo:
+        whole = self._whole  # already summarised while the upload streamed (run(arrival=...))
+        if whole is None and s.whole_hi > s.whole_lo:
             whole = ops.whole(frames_local, vec, base, T, (s.whole_lo - base, s.whole_hi - s.whole_lo),
                               corr(s.whole_lo, s.whole_hi))
         if handle is not None:
@@ -616,8 +636,8 @@ class BalancedShardedPreprocessor:
             _lib.call("vb_memset_async", pb.peer[1], 0, h * w * 8, D.stream_handle())  # the sum starts at 0
             run_piece(p, pb.peer[0], pb.peer[1])  # raw peer addresses: the kernels write the owner's memory
             tk.send(p.next)  # READY
-        whole = None
-        if s.whole_hi > s.whole_lo:
+        whole = self._whole  # already summarised while the upload streamed (run(arrival=...))
+        if whole is None and s.whole_hi > s.whole_lo:
             whole = ops.whole(frames_local, vec, base, T, (s.whole_lo - base, s.whole_hi - s.whole_lo),
                               corr(s.whole_lo, s.whole_hi))
         sp_parts, tp_parts = [], []

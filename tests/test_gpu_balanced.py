@@ -34,10 +34,35 @@ def _cfg(radius, L, m, win, shading):
                        shading_sigma=shading)
 
 
+def _streamed_run(runner, raw_local, s, m, corr, piece):
+    """The second run with the shard uploaded in pieces on a side stream and
+    run(arrival=...) waiting per piece (bench.py's strong-scaling e2e)."""
+    host = torch.from_numpy(raw_local.view(np.int16)).pin_memory()
+    dev = torch.empty(host.shape, dtype=torch.int16, device="cuda")
+    up = torch.cuda.Stream()
+    up.wait_stream(torch.cuda.current_stream())
+    evs = []
+    with torch.cuda.stream(up):
+        for a in range(0, host.shape[0], piece):
+            b = min(host.shape[0], a + piece)
+            dev[a:b].copy_(host[a:b], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(up)
+            evs.append((a, b, ev))
+
+    def arrival(a, b):
+        for x, y, ev in evs:
+            if x < b and y > a:
+                torch.cuda.current_stream().wait_event(ev)
+
+    return runner.run(dev.view(torch.uint16), s, m, corrected_out=corr, arrival=arrival, chunk=piece)
+
+
 def _worker(rank, world, port, raw, radius, L, m, win, shading, out_dir, exchange="peer"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    exchange, _, piece = exchange.partition("+stream")
     try:
         t, h, w = raw.shape
         s = distributed.balanced_plan(t, L, world, rank, win)
@@ -47,7 +72,10 @@ def _worker(rank, world, port, raw, radius, L, m, win, shading, out_dir, exchang
         # two runs: the second reuses the exchange buffers (peer mode: ACK-ordered overwrite)
         first = runner.run(local, s, m, corrected_out=corr)
         first_tp = first.temporal.clone()
-        res = runner.run(local, s, m, corrected_out=corr)
+        if piece:  # "+stream<n>": the second run streams its shard in n-frame pieces
+            res = _streamed_run(runner, np.ascontiguousarray(raw[s.local_lo:s.local_hi]), s, m, corr, int(piece))
+        else:
+            res = runner.run(local, s, m, corrected_out=corr)
         assert torch.equal(first_tp, res.temporal), "second run differs"
         vec = D.motion_to_numpy(res.vectors, res.n_frames)[s.frame_lo - s.local_lo:s.frame_hi - s.local_lo]
         np.savez(os.path.join(out_dir, f"r{rank}.npz"), vec=vec, sp=res.spatial.cpu().numpy(),
@@ -64,6 +92,9 @@ def _worker(rank, world, port, raw, radius, L, m, win, shading, out_dir, exchang
     (300, 128, 5, 100, 0, 0.0, "p2p"),
     (500, 128, 3, 100, 33, 16.0, "peer"),  # A17 high-pass halo + shading gain through the pieces
     (122, 40, 2, 100, 0, 0.0, "peer"),    # 2-frame final block
+    (600, 100, 4, 150, 0, 0.0, "peer+stream37"),  # streamed shard: search per piece, whole blocks as they complete
+    (300, 128, 5, 100, 0, 0.0, "p2p+stream50"),
+    (400, 100, 1, 150, 0, 0.0, "peer+stream64"),  # one rank: every block whole, summarised during the upload
 ])
 @pytest.mark.timeout(300)
 def test_balanced_shards_equal_single_run(cuda, tmp_path, T, L, W, m, win, shading, exchange):
