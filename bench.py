@@ -61,6 +61,8 @@ def parse():
     p.add_argument("--frames", type=int, default=0, help="override frames per rank (profiling only)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-single-thread", action="store_true",
+                   help="reference arm: skip the extra threads=1 block (BASELINE.md section 3 asks for N = 1 too)")
     p.add_argument("--no-corrected", action="store_true", help="do not materialise the corrected video")
     p.add_argument("--cpu-sample", type=int, default=2000, help="frames in the CPU baseline sample (~10 s of CPU work on C2)")
     p.add_argument("--ref-step-frames", type=int, default=0,
@@ -258,6 +260,15 @@ def run_reference(args):
     times = [step() for _ in range(args.steps)]
     total = sum(times)
     fps = n * args.steps / total
+    # also N = 1 (one block, after the timed steps)
+    one = None
+    if not args.no_single_thread and threads > 1:
+        if kind == "reference":
+            fps1 = n / reference_stage_fps(rec[:n], cfg, 1)[1]
+        else:
+            fps1 = n / oracle_port_fps(rec[:n], cfg, 1)[1]
+        one = {"value": fps1, "unit": UNIT, "cores": 1, "kind": kind,
+               "sample": f"block 0 of {cfg.name} ({n} frames) with threads=1, timed after the steps"}
     line = {
         "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
@@ -272,9 +283,28 @@ def run_reference(args):
                                    f"correct_motion(threads={threads}) + summarize(L={cfg.segment_length}); the "
                                    f"template is each block's first M frames"},
         "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline_1thread": one,
+        "host": host_details(),
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def host_details() -> dict:
+    """core count, CPU model, numpy / scipy versions."""
+    d = {"cores": os.cpu_count(), "numpy": np.__version__}
+    try:
+        import scipy
+
+        d["scipy"] = scipy.__version__
+    except ImportError:
+        d["scipy"] = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            d["cpu_model"] = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), None)
+    except OSError:
+        d["cpu_model"] = None
+    return d
 
 
 # ---------------------------------------------------------------- ours
