@@ -10,6 +10,7 @@ bit.  GPU: tests/test_gpu_balanced.py runs the same protocol on the CUDA
 entry points."""
 import os
 import socket
+from types import SimpleNamespace
 
 import numpy as np
 import pytest
@@ -74,6 +75,7 @@ class OracleOps:
         self.O = oracle_mod
         self.origins = oracle_mod.patch_grid(h, w, 21, radius)
         self.radius, self.L = radius, L
+        self.cfg = SimpleNamespace(segment_length=L)
 
     def template(self, frames, lo, hi, m, group):
         tsum = torch.zeros(frames.shape[1:], dtype=torch.float64)
@@ -82,9 +84,18 @@ class OracleOps:
         distributed.allreduce_sum_(tsum, group)
         self.ref = (tsum.numpy() / m).astype(np.float32)
 
-    def estimate(self, frames):
-        return np.array([self.O.estimate_motion(f.numpy(), self.ref, self.origins, 21, self.radius)
-                         for f in frames], dtype=np.float64).reshape(-1, 5)
+    def estimate(self, frames, arrival=None, chunk=0, after=None):
+        vec = np.zeros((frames.shape[0], 5), np.float64)
+        step = chunk if arrival is not None and chunk > 0 else frames.shape[0]
+        for a in range(0, frames.shape[0], max(step, 1)):
+            b = min(frames.shape[0], a + step)
+            if arrival is not None:
+                arrival(a, b)
+            vec[a:b] = np.array([self.O.estimate_motion(f.numpy(), self.ref, self.origins, 21, self.radius)
+                                 for f in frames[a:b]], dtype=np.float64).reshape(-1, 5)
+            if after is not None:
+                after(vec, b)
+        return vec
 
     @staticmethod
     def vec_slice(vec, a, b):
@@ -136,7 +147,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, raw, L, m, radius, out_dir):
+def _worker(rank, world, port, raw, L, m, radius, out_dir, piece=0):
     from oracle import oracle as O
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -148,21 +159,35 @@ def _worker(rank, world, port, raw, L, m, radius, out_dir):
         runner = distributed.BalancedShardedPreprocessor(h, w, ops=ops)
         local = torch.from_numpy(raw[s.local_lo:s.local_hi].astype(np.float32))
         corr = torch.empty((s.frames, h, w), dtype=torch.float32)
-        res = runner.run(local, s, m, corrected_out=corr)
+        if piece:  # streamed upload protocol: arrival(a, b) requests, in order, before use
+            asked = []
+            res = runner.run(local, s, m, corrected_out=corr, arrival=lambda a, b: asked.append((a, b)),
+                             chunk=piece)
+            n = s.local_hi - s.local_lo
+            pieces = [(a, min(n, a + piece)) for a in range(0, n, piece)]
+            assert asked[-1] == (0, n) and asked[-1 - len(pieces):-1] == pieces, asked
+            assert len(asked) in (len(pieces) + 1, len(pieces) + 2)  # + the template rows, if any
+            if len(asked) == len(pieces) + 2:
+                assert 0 <= asked[0][0] < asked[0][1] <= n
+        else:
+            res = runner.run(local, s, m, corrected_out=corr)
         np.savez(os.path.join(out_dir, f"r{rank}.npz"), vec=res.vectors, sp=res.spatial.numpy(),
                  tp=res.temporal.numpy(), corr=corr.numpy(), lo=s.block_lo, hi=s.block_hi)
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("T,L,W,m", [(122, 40, 2, 100), (100, 30, 3, 50), (90, 60, 4, 20)])
-def test_balanced_protocol_matches_oracle(tmp_path, oracle_mod, T, L, W, m):
+@pytest.mark.parametrize("T,L,W,m,piece", [(122, 40, 2, 100, 0), (100, 30, 3, 50, 0), (90, 60, 4, 20, 0),
+                                            (122, 40, 2, 100, 7), (100, 30, 1, 50, 13)])
+def test_balanced_protocol_matches_oracle(tmp_path, oracle_mod, T, L, W, m, piece):
     """Sharded (gloo, W ranks, blocks straddling ranks -- incl. a block spread
-    over three ranks for (90, 60, 4)) == oracle.preprocess of the whole recording."""
+    over three ranks for (90, 60, 4)) == oracle.preprocess of the whole recording;
+    piece > 0: the streamed-upload protocol (run(arrival=..., chunk=piece):
+    search per piece, whole blocks summarised as they complete)."""
     cfg = synth.CONFIGS["c1"].with_frames(T)
     raw = synth.generate_numpy(cfg)
     radius = cfg.radius
-    mp.start_processes(_worker, args=(W, _free_port(), raw, L, m, radius, str(tmp_path)), nprocs=W,
+    mp.start_processes(_worker, args=(W, _free_port(), raw, L, m, radius, str(tmp_path), piece), nprocs=W,
                        start_method="spawn")
     want = oracle_mod.preprocess(raw.astype(np.float32), 21, radius, True, m, L, 3.0)
     sp, tp, corr, vec = {}, {}, [], []
