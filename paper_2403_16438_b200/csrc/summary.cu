@@ -895,7 +895,10 @@ __global__ void block_mean_kernel(const float* __restrict__ frames, int64_t n, i
 }
 
 // ------------------------------------------------------------------ K4
-constexpr int kK4Pix = 16, kK4Threads = 256;
+#ifndef VB_K4_PIX
+#define VB_K4_PIX 16
+#endif
+constexpr int kK4Pix = VB_K4_PIX, kK4Threads = 256;  // pixels per median CTA (multiple of 4)
 constexpr int kMaxHalfWindow = 512;  // high-pass window N = 2*hh+1 <= 1025 frames
 
 // Order-preserving uint32 key of a float32 (total order, -0 < +0): selection
@@ -1090,7 +1093,7 @@ __global__ void __launch_bounds__(kK4Threads) median_kernel(K4Args a) {
 #pragma unroll
             for (int j = 0; j < kB; ++j) {
                 const int i = i0 + j * kK4Threads;
-                const int tt = i >> 2, q = i & 3;
+                const int tt = i / (kK4Pix / 4), q = i % (kK4Pix / 4);
                 int64_t g = t0 - hh + tt;
                 if constexpr (HP) g = reflect64(g, a.t_total);
                 vals[j] = i < total4 ? __ldcs(reinterpret_cast<const float4*>(a.sm + (g - a.s_lo) * a.hw + p0) + q)
@@ -1100,7 +1103,7 @@ __global__ void __launch_bounds__(kK4Threads) median_kernel(K4Args a) {
             for (int j = 0; j < kB; ++j) {
                 const int i = i0 + j * kK4Threads;
                 if (i < total4) {
-                    float* d = sm4 + (i >> 2) * ST + (i & 3) * 4;
+                    float* d = sm4 + (i / (kK4Pix / 4)) * ST + (i % (kK4Pix / 4)) * 4;
                     d[0] = vals[j].x;
                     d[1] = vals[j].y;
                     d[2] = vals[j].z;
