@@ -545,10 +545,12 @@ class BalancedShardedPreprocessor:
             # whole blocks are summarised as soon as their frames are searched,
             # while later pieces are still uploading
             wl, wh, L = s.whole_lo - base, s.whole_hi - base, ops.cfg.segment_length
+            # the temporal high-pass (A17) reads window // 2 frames past a block's end
+            halo = max(0, int(getattr(getattr(ops, "pre", None), "window", 0) or 0)) // 2
             parts, done = [], [wl]
 
             def after(vec, b):
-                while done[0] < wh and min(done[0] + L, wh) <= b:
+                while done[0] < wh and (min(done[0] + L, wh) + halo <= b or b == n_local):
                     e = min(done[0] + L, wh)
                     parts.append(ops.whole(frames_local, vec, base, T, (done[0], e - done[0]),
                                            corr(done[0] + base, e + base)))

@@ -95,6 +95,8 @@ def _worker(rank, world, port, raw, radius, L, m, win, shading, out_dir, exchang
     (600, 100, 4, 150, 0, 0.0, "peer+stream37"),  # streamed shard: search per piece, whole blocks as they complete
     (300, 128, 5, 100, 0, 0.0, "p2p+stream50"),
     (400, 100, 1, 150, 0, 0.0, "peer+stream64"),  # one rank: every block whole, summarised during the upload
+    (500, 128, 3, 100, 33, 16.0, "peer+stream40"),  # streamed with the A17 halo: a block waits for its halo
+    (500, 128, 1, 100, 33, 0.0, "p2p+stream64"),  # pieces end on block ends: the halo must still be waited for
 ])
 @pytest.mark.timeout(300)
 def test_balanced_shards_equal_single_run(cuda, tmp_path, T, L, W, m, win, shading, exchange):
