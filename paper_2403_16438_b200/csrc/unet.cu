@@ -368,6 +368,15 @@ __global__ void __launch_bounds__(128) conv3x3_tc_kernel(ConvArgs a) {
                 }
                 if (ox0 > 0) rows[k][0] = __ldg(src + ox0 - 1);
                 if (ox0 + kTcTW < a.w) rows[k][kTcPW - 1] = __ldg(src + ox0 + kTcTW);
+            } else if (step == 2) {  // nearest upsample: 8 low-res samples (two float4, each used twice) + halo
+                const int lx0 = ox0 >> 1;  // a multiple of 8: aligned
+                const float4* v4 = reinterpret_cast<const float4*>(src + lx0);
+                const float4 t0 = __ldg(v4), t1 = __ldg(v4 + 1);
+                const float lr[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+#pragma unroll
+                for (int j = 0; j < 8; ++j) rows[k][1 + 2 * j] = rows[k][2 + 2 * j] = lr[j];
+                if (ox0 > 0) rows[k][0] = __ldg(src + lx0 - 1);
+                if (ox0 + kTcTW < a.w) rows[k][kTcPW - 1] = __ldg(src + lx0 + kTcTW / 2);
             } else {
 #pragma unroll
                 for (int j = 0; j < kTcPW; ++j) {
