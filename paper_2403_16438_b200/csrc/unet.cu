@@ -402,14 +402,14 @@ __global__ void __launch_bounds__(128) conv3x3_tc_kernel(ConvArgs a) {
             }
         }
     };
+    // the chunk's pre-split weights: one bulk copy issued by thread 0, completing on bar[1]
     auto fetch_w = [&](int ch) {
-        const float* wsrc = a.wtc + (size_t)ch * (2 * kWBytes / 4);
-        for (int i = tid; i < 2 * kWBytes / 16; i += 128)
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(tc_smem + 4 * kTcPlane + i * 16)),
-                         "l"(wsrc + i * 4)
-                         : "memory");
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        if (tid == 0) {
+            mbar_expect_tx(&bar[1], 2 * kWBytes);
+            bulk_load(tc_smem + 4 * kTcPlane, a.wtc + (size_t)ch * (2 * kWBytes / 4), 2 * kWBytes, &bar[1]);
+        }
     };
+    uint32_t wph = 0;
     auto issue = [&](int ch) {
         const uint32_t sb = smem_u32(tc_smem);
         constexpr uint32_t idesc = umma_idesc_tf32(128, N);
@@ -449,8 +449,11 @@ __global__ void __launch_bounds__(128) conv3x3_tc_kernel(ConvArgs a) {
         if (dbg != 2) {
             fetch_w(ch);
             store_rows();
+            if (tid == 0) {  // only the MMA-issuing thread reads the weights (async proxy, after this wait)
+                mbar_wait(&bar[1], wph);
+                wph ^= 1u;
+            }
         }
-        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;\n");
         __syncthreads();
