@@ -48,7 +48,15 @@ def _dtype(bps: int, sfmt: int, order: str) -> np.dtype:
 
 
 def _pages(buf) -> list[_Page]:
-    """Parse the IFD chain of a TIFF in `buf` (bytes-like or np.memmap)."""
+    """Parse the IFD chain of a TIFF in `buf` (bytes-like or np.memmap);
+    truncated structures raise TiffError."""
+    try:
+        return _parse(buf)
+    except struct.error as exc:
+        raise TiffError(f"truncated TIFF structure ({exc})") from None
+
+
+def _parse(buf) -> list[_Page]:
     if len(buf) < 8:
         raise TiffError("file too short")
     bo = bytes(buf[:2])

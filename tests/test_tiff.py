@@ -136,3 +136,21 @@ def test_load_save_video_tiff_like_reference(tmp_path):
     np.testing.assert_array_equal(io.load_video(tmp_path / "b.tiff").data, raw.astype(np.float32))
     rec = io.open_recording(tmp_path / "b.tiff")
     assert isinstance(rec, np.memmap) and rec.dtype == np.uint16
+
+
+def test_truncated_files_raise_tiff_error(tmp_path):
+    """Cuts anywhere in the file (inside an IFD entry, past the strips, in
+    the header) raise TiffError, never a bare struct / index error; a cut
+    that only drops the final IFD's alignment padding still reads back."""
+    p = tmp_path / "a.tif"
+    want = (np.arange(2 * 8 * 8) % 65535).astype(np.uint16).reshape(2, 8, 8)
+    tiff.write_tiff(p, want)
+    data = p.read_bytes()
+    for cut in list(range(0, len(data), 7)) + [len(data) - 1]:
+        q = tmp_path / "cut.tif"
+        q.write_bytes(data[:cut])
+        try:
+            got = tiff.read_tiff(q, mmap=False)
+        except tiff.TiffError:
+            continue
+        np.testing.assert_array_equal(got, want)
